@@ -1,0 +1,364 @@
+#!/usr/bin/env python3
+"""bench.py -- block-sparse FP64 useful GFLOP/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[0], the config the metric is quoted on:
+"10% occupancy with 23x23 blocks"): C += A*B with A, B 400 x 400 blocks of
+23 x 23 (N = 9,200), 10 % random block occupancy, C_in empty, eps = 0.
+Synthetic inputs: block presence Bernoulli(0.10), values N(0,1), seeded
+(A: 1001, B: 1002) with numpy's PCG64 so both arms regenerate identical inputs.
+
+A "step" = one full multiply call (stack generation, symbolic C pattern,
+small-GEMM numeric phase, C install).  N > 1 (torchrun, one process per GPU):
+weak scaling over a row-slab distribution -- every rank owns 400 block-rows of
+A and C (a 400*N x 400 A), B (400 x 400 blocks) is K-sliced across ranks and
+circulates over NCCL in a ring (the reference's multiply_virtual_case2
+schedule, multiply_rect.hpp:199-238), so per-rank work equals the N = 1 step.
+
+Impls:
+  (default)          the B200 product through its C-ABI (libbtcuda.so)
+  --impl reference   the reference's own CPU path (oracle/_ref, compiled from the
+                     unmodified /root/reference headers) on the box's host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NB, BS, OCC = 400, 23, 0.10
+SEED_A, SEED_B = 1001, 1002
+FP64_PEAK_TFLOPS = 37.1   # measured: tools/microbench/fp64_peak.cu on B200 (profiles/)
+
+
+# --------------------------------------------------------------- inputs
+def make_blocks(seed: int, nbr: int, nbc: int, bs: int, occ: float, row0: int = 0):
+    """Canonical (bi, bj, vals) block list, Bernoulli(occ) presence, N(0,1) values.
+    Rows [row0, row0+nbr) of a conceptually larger matrix (row-sliced seeding keeps
+    every rank's slab independent of the world size)."""
+    bis, bjs, vs = [], [], []
+    for r in range(row0, row0 + nbr):
+        g = np.random.default_rng([seed, r])
+        mask = g.random(nbc) < occ
+        js = np.nonzero(mask)[0].astype(np.int64)
+        bis.append(np.full(len(js), r - row0, np.int64))
+        bjs.append(js)
+        vs.append(g.standard_normal(len(js) * bs * bs))
+    return np.concatenate(bis), np.concatenate(bjs), np.concatenate(vs)
+
+
+def useful_flops_host(a_bi, a_bj, b_bi, b_bj, bs):
+    """2*m*n*k per (i,k,j) with A_ik and B_kj stored."""
+    b_rows = np.bincount(b_bi, minlength=NB)
+    return 2.0 * bs ** 3 * float(b_rows[a_bj].sum())
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    """The reference's own CPU implementation (oracle/_ref/libbtref.so) on this box's
+    host cores: multiply_cannon on the largest square grid <= nproc (one
+    std::thread per simulated rank, comm.hpp:273-290)."""
+    if rank != 0:
+        return None
+    from oracle.oracle import Blocks, Reference  # the one place bench runs oracle/
+    ref = Reference()
+    cores = os.cpu_count() or 1
+    q = int(np.floor(np.sqrt(cores)))
+    sz = np.full(NB, BS, np.int32)
+    abi, abj, av = make_blocks(SEED_A, NB, NB, BS, OCC)
+    bbi, bbj, bv = make_blocks(SEED_B, NB, NB, BS, OCC)
+    A = Blocks(sz, sz, abi, abj, av)
+    B = Blocks(sz, sz, bbi, bbj, bv)
+    C = Blocks.empty(sz, sz)
+    flops = useful_flops_host(abi, abj, bbi, bbj, BS)
+    for _ in range(args.warmup):
+        ref.multiply(A, B, C, "cannon", q, q * q)
+    times = []
+    for _ in range(args.steps):
+        _, secs, _ = ref.multiply(A, B, C, "cannon", q, q * q)
+        times.append(secs)
+    t = float(np.sum(times))
+    val = flops * args.steps / t / 1e9
+    line = {
+        "impl": "reference", "metric": "block-sparse FP64 useful GFLOP/s",
+        "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Bernoulli presence, N(0,1) values)",
+        "config": {"workload": "c1: 400x400 blocks of 23x23 (N=9200), occ 0.10, eps 0",
+                   "algorithm": f"reference multiply_cannon on a {q}x{q} simulated grid"},
+        "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": q * q,
+                         "kind": "reference",
+                         "sample": f"full c1 instance per step ({flops/1e9:.2f} GFLOP)"},
+        "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def cpu_baseline_sample():
+    """cpu_baseline for the product line: the reference on ONE core (1x1 Cannon),
+    one full c1 instance (~9-15 s of CPU work)."""
+    from oracle.oracle import Blocks, Reference
+    ref = Reference()
+    sz = np.full(NB, BS, np.int32)
+    abi, abj, av = make_blocks(SEED_A, NB, NB, BS, OCC)
+    bbi, bbj, bv = make_blocks(SEED_B, NB, NB, BS, OCC)
+    flops = useful_flops_host(abi, abj, bbi, bbj, BS)
+    out, secs, _ = ref.multiply(Blocks(sz, sz, abi, abj, av), Blocks(sz, sz, bbi, bbj, bv),
+                                Blocks.empty(sz, sz), "cannon", 1, 1)
+    return {"value": round(flops / secs / 1e9, 3), "unit": "GFLOP/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"one full c1 instance, reference multiply_cannon 1x1 grid "
+                      f"({flops/1e9:.2f} GFLOP in {secs:.2f} s)"}, out
+
+
+# --------------------------------------------------------------- product
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--check", action="store_true", help="verify C against the reference")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1910_13555_b200.store import Context, LocalStore, multiply_local, unique_id
+    if world > 1:
+        from paper_1910_13555_b200 import dist as ring
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = Context(local, world, rank, obj[0])
+    else:
+        ctx = Context(local)
+    ctx.set_timing(True)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    sz = np.full(NB, BS, np.int32)
+
+    # ---- inputs (host, pinned) -- A/C row slab of this rank, B K-slab of this rank
+    abi, abj, av = make_blocks(SEED_A, NB, NB, BS, OCC, row0=NB * rank)
+    chunk = -(-NB // world)   # ChunkPartition (partition.hpp:17-41)
+    kslab = [(min(NB, chunk * p), min(NB, chunk * (p + 1))) for p in range(world)]
+    k0, k1 = kslab[rank]
+    bbi_all, bbj_all, bv_all = make_blocks(SEED_B, NB, NB, BS, OCC)
+    sel = (bbi_all >= k0) & (bbi_all < k1)
+    bsize = BS * BS
+    bidx = np.nonzero(sel)[0]
+    bbi, bbj = bbi_all[sel], bbj_all[sel]
+    bv = bv_all.reshape(-1, bsize)[bidx].ravel()
+    av_pin = torch.from_numpy(av).pin_memory()
+    bv_pin = torch.from_numpy(np.ascontiguousarray(bv)).pin_memory()
+
+    a = LocalStore(ctx, sz, sz)
+    a.put_blocks(abi, abj, av_pin)
+    b = LocalStore(ctx, sz, sz)
+    b.put_blocks(bbi, bbj, bv_pin)
+    c = LocalStore(ctx, sz, sz)
+    flops_rank = useful_flops_host(abi, abj, bbi_all, bbj_all, BS)
+
+    def step(cc):
+        cc.clear()
+        if world == 1:
+            return multiply_local(ctx, a, b, cc)
+        return ring.multiply_gather_b(ctx, a, b, cc)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        st = step(c)
+    ctx.sync()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    k_before = ctx.kernel_count
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    ms_numeric = []
+    stats = []
+    with ClockSampler(local) as clocks:
+        for s in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()                       # L2 flush, outside the timed events
+                ev[s][0].record(stream)
+            st = step(c)
+            with torch.cuda.stream(stream):
+                ev[s][1].record(stream)
+            ms_numeric.append(st["ms_numeric"])
+            stats.append(st)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    kernels = ctx.kernel_count - k_before
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    ms_local = float(np.mean(step_ms))
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops_step = stats[-1]["flops"]
+    assert abs(flops_step - flops_rank) <= 1e-6 * flops_rank, (flops_step, flops_rank)
+    value = flops_step * world / (ms * 1e-3) / 1e9     # whole-job GFLOP/s
+
+    # ---- dominant kernel roofline (small-GEMM numeric phase, live CUDA events)
+    kn_ms = float(np.mean(ms_numeric))
+    achieved = flops_step / (kn_ms * 1e-3) / 1e12
+
+    # ---- e2e through the public API with host buffers (rank-local)
+    e2e_times = []
+    cout = torch.empty(NB * NB * bsize, dtype=torch.float64).pin_memory()
+    h2d = av.nbytes + bv.nbytes + 16 * (len(abi) + len(bbi))
+    d2h = 0
+    for s in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ea = LocalStore(ctx, sz, sz)
+        ea.put_blocks(abi, abj, av_pin)
+        eb = LocalStore(ctx, sz, sz)
+        eb.put_blocks(bbi, bbj, bv_pin)
+        ec = LocalStore(ctx, sz, sz)
+        if world == 1:
+            multiply_local(ctx, ea, eb, ec)
+        else:
+            ring.multiply_gather_b(ctx, ea, eb, ec)
+        ci, cj, _ = ec.export(cout)
+        ctx.sync()
+        dt = time.perf_counter() - t0
+        d2h = 8 * int(ec.info()[1]) + 16 * len(ci)
+        for x in (ea, eb, ec):
+            x.close()
+        if s >= args.warmup:
+            e2e_times.append(dt)
+    e2e_s = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = flops_step * world / e2e_s / 1e9
+
+    if rank == 0:
+        line = {
+            "metric": "block-sparse FP64 useful GFLOP/s",
+            "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Bernoulli(0.10) block presence, N(0,1) values)",
+            "config": {
+                "workload": "c1: 400x400 blocks of 23x23 (N=9200) per rank, occ 0.10, "
+                            "C_in empty, eps 0",
+                "products_per_rank": int(stats[-1]["products"]),
+                "useful_gflop_per_rank": round(flops_step / 1e9, 4),
+                "distribution": "single GPU" if world == 1 else
+                f"A/C row slabs per rank, B K-slab ring over NCCL ({world} ranks)",
+                "l2": "flushed (256 MB write) before every timed step",
+            },
+            "roofline": {
+                "bound": "tensor", "achieved": round(achieved, 3),
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
+                "kernel": "k_smm_dmma<3,3,4> (FP64 DMMA 8x8x4 small-GEMM)",
+                "peak_source": "measured FP64 DMMA/DFMA peak on B200 "
+                               "(profiles/fp64_peak_r01.txt)",
+                "step_share": round(kn_ms / ms_local, 3),
+            },
+            "e2e": {"value": round(e2e_val, 2), "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(kernels),
+            "clocks": clocks.summary(),
+        }
+        if not args.no_cpu_baseline:
+            cb, _ = cpu_baseline_sample()
+            line["cpu_baseline"] = cb
+        print(json.dumps(line), flush=True)
+    for x in (a, b, c):
+        x.close()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

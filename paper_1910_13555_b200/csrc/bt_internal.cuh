@@ -1,0 +1,155 @@
+// bt_internal.cuh -- shared internals of libbtcuda (device BCSR store, context,
+// error plumbing).  See DESIGN.md section 2 for the HBM layout.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "btcuda.h"
+
+namespace bt {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define BT_CUDA(x)                                                                         \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::bt::Error(e_ == cudaErrorMemoryAllocation ? BT_ERR_OOM : BT_ERR_CUDA,        \
+                        std::string("CUDA error ") + cudaGetErrorString(e_) + " at " +     \
+                            __FILE__ + ":" + std::to_string(__LINE__));                    \
+  } while (0)
+
+#define BT_REQUIRE(cond, code, msg) \
+  do {                              \
+    if (!(cond)) throw ::bt::Error((code), (msg)); \
+  } while (0)
+
+// wraps a C-ABI body: converts exceptions to status codes + bt_last_error()
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return BT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return BT_ERR_OOM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return BT_ERR_INTERNAL;
+  }
+}
+
+// ------------------------------------------------------------------ memory
+// Stream-ordered device buffer from the device's default mempool (release
+// threshold raised at context creation, so steady-state multiplies never hit
+// cudaMalloc).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p; n = o.n; s = o.s;
+      o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) BT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+// ----------------------------------------------------------------- context
+struct Ctx {
+  int device = 0;
+  int nranks = 1;
+  int rank = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  int64_t kernels = 0;  // kernels launched through this context
+  void* nccl = nullptr; // ncclComm_t when nranks > 1
+  DBuf<unsigned char> scratch;  // CUB temp storage, reused
+  void* pinned = nullptr;       // small pinned host staging for scalar readbacks
+  bool timing = false;          // record CUDA events around multiply kernels
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* ensure_scratch(size_t bytes);
+};
+
+// ------------------------------------------------------------------- store
+// One rank's block-CSR store, device resident:
+//   row_ptr[nbr+1] int32 over ALL block rows (dense row pointer),
+//   col[nblk]      int32 global block column, strictly increasing per row,
+//   off[nblk]      int64 element offset of the block in vals; every block slot is
+//                  padded to an even element count so each starts 16-byte aligned
+//                  (cp.async.bulk / vector access),
+//   vals           padded FP64 slab, row-major m x n blocks.
+struct Mat {
+  Ctx* ctx = nullptr;
+  int64_t nbr = 0, nbc = 0;
+  std::vector<int32_t> h_rsz, h_csz;
+  DBuf<int32_t> rsz, csz;
+  int32_t max_r = 0, max_c = 0;
+  bool uniform_r = true, uniform_c = true;
+  int64_t nblk = 0;
+  int64_t nelems = 0;  // stored (unpadded) elements
+  int64_t nvals = 0;   // padded slab length
+  DBuf<int32_t> row_ptr;
+  DBuf<int32_t> col;
+  DBuf<int64_t> off;
+  DBuf<double> vals;
+  cudaStream_t stream() const { return ctx->stream; }
+  void init_empty();  // empty pattern (row_ptr all zero)
+};
+
+__host__ __device__ inline int64_t pad2(int64_t x) { return (x + 1) & ~int64_t(1); }
+
+// launch accounting
+inline void count_launch(Ctx* c, int n = 1) { c->kernels += n; }
+
+// implemented in bt_store.cu
+__global__ void k_block_norms(const double* vals, const int32_t* row_ptr, const int32_t* col,
+                              const int64_t* off, const int32_t* rsz, const int32_t* csz,
+                              int64_t nbr, double* out, int64_t nblk);
+void upload_sizes(Mat& m);
+void check_launch(const char* what);
+
+}  // namespace bt
+
+struct bt_ctx {
+  bt::Ctx impl;
+};
+struct bt_mat {
+  bt::Mat impl;
+};

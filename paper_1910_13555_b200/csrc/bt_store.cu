@@ -1,0 +1,613 @@
+// bt_store.cu -- context and device block-CSR store (LocalStore equivalent).
+//
+// Reference: matrix.hpp:137-275 (LocalStore), :279-401 (DistMatrix put/get),
+// :404-418 (new_matrix).  The store is device resident; host buffers only
+// cross the boundary inside put/export/get calls.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "bt_internal.cuh"
+
+namespace bt {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    throw Error(BT_ERR_CUDA, std::string("kernel launch failed (") + what + "): " +
+                                 cudaGetErrorString(e));
+}
+
+void* Ctx::ensure_scratch(size_t bytes) {
+  if (scratch.n < bytes) scratch.alloc(std::max(bytes, size_t(1) << 20), stream);
+  return scratch.p;
+}
+
+void upload_sizes(Mat& m) {
+  m.rsz.alloc(std::max<int64_t>(m.nbr, 1), m.stream());
+  m.csz.alloc(std::max<int64_t>(m.nbc, 1), m.stream());
+  if (m.nbr)
+    BT_CUDA(cudaMemcpyAsync(m.rsz.p, m.h_rsz.data(), sizeof(int32_t) * m.nbr,
+                            cudaMemcpyHostToDevice, m.stream()));
+  if (m.nbc)
+    BT_CUDA(cudaMemcpyAsync(m.csz.p, m.h_csz.data(), sizeof(int32_t) * m.nbc,
+                            cudaMemcpyHostToDevice, m.stream()));
+  m.max_r = m.nbr ? *std::max_element(m.h_rsz.begin(), m.h_rsz.end()) : 0;
+  m.max_c = m.nbc ? *std::max_element(m.h_csz.begin(), m.h_csz.end()) : 0;
+  m.uniform_r = m.nbr == 0 || std::all_of(m.h_rsz.begin(), m.h_rsz.end(),
+                                          [&](int32_t s) { return s == m.h_rsz[0]; });
+  m.uniform_c = m.nbc == 0 || std::all_of(m.h_csz.begin(), m.h_csz.end(),
+                                          [&](int32_t s) { return s == m.h_csz[0]; });
+}
+
+void Mat::init_empty() {
+  nblk = 0;
+  nelems = 0;
+  nvals = 0;
+  col.release();
+  off.release();
+  vals.release();
+  row_ptr.alloc(nbr + 1, stream());
+  BT_CUDA(cudaMemsetAsync(row_ptr.p, 0, sizeof(int32_t) * (nbr + 1), stream()));
+}
+
+// ----------------------------------------------------------------- kernels
+// One warp per block: copy a padded slot (even length, 16-byte aligned on both
+// sides) with 16-byte vector accesses.
+__global__ void k_gather_blocks(double* __restrict__ dst, const int64_t* __restrict__ dst_off,
+                                const double* __restrict__ src,
+                                const int64_t* __restrict__ src_off,
+                                const int64_t* __restrict__ len, int64_t n) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const int64_t so = src_off[w];
+  if (so < 0) return;
+  const double2* s = reinterpret_cast<const double2*>(src + so);
+  double2* d = reinterpret_cast<double2*>(dst + dst_off[w]);
+  const int64_t n2 = pad2(len[w]) >> 1;
+  for (int64_t t = lane; t < n2; t += 32) d[t] = s[t];
+}
+
+// Put plan application: output block w = base (old slot or first input) +
+// remaining inputs in batch order (LocalStore::insert accumulate semantics,
+// matrix.hpp:176-179).
+__global__ void k_apply_put(double* __restrict__ dst, const int64_t* __restrict__ dst_off,
+                            const int64_t* __restrict__ len, const double* __restrict__ old,
+                            const int64_t* __restrict__ old_off,
+                            const double* __restrict__ inp, const int64_t* __restrict__ inp_ptr,
+                            const int64_t* __restrict__ inp_src, int64_t n) {
+  const int64_t w = blockIdx.x;
+  if (w >= n) return;
+  const int64_t L = len[w];
+  double* d = dst + dst_off[w];
+  const int64_t oo = old_off[w];
+  const int64_t i0 = inp_ptr[w], i1 = inp_ptr[w + 1];
+  for (int64_t e = threadIdx.x; e < L; e += blockDim.x) {
+    double v;
+    int64_t t = i0;
+    if (oo >= 0) {
+      v = old[oo + e];
+    } else {
+      v = inp[inp_src[t] + e];
+      ++t;
+    }
+    for (; t < i1; ++t) v = __dadd_rn(v, inp[inp_src[t] + e]);
+    d[e] = v;
+  }
+}
+
+// padded slot -> compact host-order slot
+__global__ void k_compact(double* __restrict__ dst, const int64_t* __restrict__ dst_off,
+                          const double* __restrict__ src, const int64_t* __restrict__ src_off,
+                          const int64_t* __restrict__ len, int64_t n) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const double* s = src + src_off[w];
+  double* d = dst + dst_off[w];
+  const int64_t L = len[w];
+  for (int64_t t = lane; t < L; t += 32) d[t] = s[t];
+}
+
+// Frobenius norm per block: sequential sum of squares, unfused.
+__global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __restrict__ row_ptr,
+                              const int32_t* __restrict__ col, const int64_t* __restrict__ off,
+                              const int32_t* __restrict__ rsz, const int32_t* __restrict__ csz,
+                              int64_t nbr, double* __restrict__ out, int64_t nblk) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= nblk) return;
+  // row of entry b: binary search in row_ptr
+  int64_t lo = 0, hi = nbr;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (row_ptr[mid] <= b) lo = mid; else hi = mid;
+  }
+  const int64_t L = (int64_t)rsz[lo] * csz[col[b]];
+  const double* p = vals + off[b];
+  double s = 0.0;
+  for (int64_t t = 0; t < L; ++t) s = __dadd_rn(s, __dmul_rn(p[t], p[t]));
+  out[b] = __dsqrt_rn(s);
+}
+
+// ------------------------------------------------------------- host helpers
+struct HostIndex {
+  std::vector<int32_t> row_ptr, col;
+  std::vector<int64_t> off;
+};
+
+static HostIndex download_index(const Mat& m) {
+  HostIndex h;
+  h.row_ptr.resize(m.nbr + 1);
+  h.col.resize(m.nblk);
+  h.off.resize(m.nblk);
+  BT_CUDA(cudaMemcpyAsync(h.row_ptr.data(), m.row_ptr.p, sizeof(int32_t) * (m.nbr + 1),
+                          cudaMemcpyDeviceToHost, m.stream()));
+  if (m.nblk) {
+    BT_CUDA(cudaMemcpyAsync(h.col.data(), m.col.p, sizeof(int32_t) * m.nblk,
+                            cudaMemcpyDeviceToHost, m.stream()));
+    BT_CUDA(cudaMemcpyAsync(h.off.data(), m.off.p, sizeof(int64_t) * m.nblk,
+                            cudaMemcpyDeviceToHost, m.stream()));
+  }
+  BT_CUDA(cudaStreamSynchronize(m.stream()));
+  return h;
+}
+
+template <class T>
+static DBuf<T> upload(const std::vector<T>& v, cudaStream_t s) {
+  DBuf<T> d(std::max<size_t>(v.size(), 1), s);
+  if (!v.empty())
+    BT_CUDA(cudaMemcpyAsync(d.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, s));
+  return d;
+}
+
+// Installs a new pattern whose values are produced by `fill` into a fresh slab.
+static void install_pattern(Mat& m, const std::vector<int32_t>& row_ptr,
+                            const std::vector<int32_t>& col, const std::vector<int64_t>& off,
+                            int64_t nvals, int64_t nelems) {
+  m.row_ptr = upload(row_ptr, m.stream());
+  m.col = upload(col, m.stream());
+  m.off = upload(off, m.stream());
+  m.nblk = static_cast<int64_t>(col.size());
+  m.nvals = nvals;
+  m.nelems = nelems;
+}
+
+static void check_mat(const bt_mat* m) {
+  BT_REQUIRE(m != nullptr, BT_ERR_INVALID_ARGUMENT, "null matrix handle");
+}
+
+}  // namespace bt
+
+using namespace bt;
+
+extern "C" {
+
+const char* bt_last_error(void) { return g_last_error.c_str(); }
+int bt_version(void) { return 1; }
+
+int bt_get_unique_id(void* id128) {
+  return guard([&] {
+    BT_REQUIRE(id128, BT_ERR_INVALID_ARGUMENT, "null id buffer");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "nccl id size");
+    std::memcpy(id128, &id, 128);
+  });
+}
+
+int bt_ctx_create(int device, int nranks, int rank, const void* nccl_id, bt_ctx** out) {
+  return guard([&] {
+    BT_REQUIRE(out, BT_ERR_INVALID_ARGUMENT, "null output handle");
+    BT_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, BT_ERR_INVALID_ARGUMENT,
+               "bt_ctx_create: bad rank/nranks");
+    BT_REQUIRE(nranks == 1 || nccl_id, BT_ERR_INVALID_ARGUMENT,
+               "bt_ctx_create: nranks > 1 needs an NCCL unique id");
+    int ndev = 0;
+    BT_CUDA(cudaGetDeviceCount(&ndev));
+    BT_REQUIRE(device >= 0 && device < ndev, BT_ERR_INVALID_ARGUMENT,
+               "bt_ctx_create: device " + std::to_string(device) + " not present (" +
+                   std::to_string(ndev) + " visible)");
+    BT_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    BT_CUDA(cudaGetDeviceProperties(&prop, device));
+    BT_REQUIRE(prop.major == 10, BT_ERR_CUDA,
+               std::string("libbtcuda is built for sm_100a (B200); device is ") + prop.name);
+    auto* c = new bt_ctx;
+    Ctx& x = c->impl;
+    x.device = device;
+    x.nranks = nranks;
+    x.rank = rank;
+    x.num_sms = prop.multiProcessorCount;
+    x.smem_optin = prop.sharedMemPerBlockOptin;
+    BT_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    BT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    BT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    BT_CUDA(cudaMallocHost(&x.pinned, 4096));
+    for (auto& e : x.ev) BT_CUDA(cudaEventCreate(&e));
+    if (nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, 128);
+      ncclComm_t comm;
+      ncclResult_t r = ncclCommInitRank(&comm, nranks, id, rank);
+      if (r != ncclSuccess) {
+        cudaStreamDestroy(x.stream);
+        delete c;
+        throw Error(BT_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      }
+      x.nccl = comm;
+    }
+    *out = c;
+  });
+}
+
+int bt_ctx_destroy(bt_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    Ctx& x = c->impl;
+    cudaSetDevice(x.device);
+    cudaStreamSynchronize(x.stream);
+    x.scratch.release();
+    cudaStreamSynchronize(x.stream);
+    if (x.nccl) ncclCommDestroy(static_cast<ncclComm_t>(x.nccl));
+    if (x.pinned) cudaFreeHost(x.pinned);
+    for (auto& e : x.ev)
+      if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(x.stream);
+    delete c;
+  });
+}
+
+int bt_ctx_sync(bt_ctx* c) {
+  return guard([&] {
+    BT_REQUIRE(c, BT_ERR_INVALID_ARGUMENT, "null context");
+    BT_CUDA(cudaStreamSynchronize(c->impl.stream));
+  });
+}
+
+int bt_ctx_rank(const bt_ctx* c, int* rank, int* nranks) {
+  return guard([&] {
+    BT_REQUIRE(c, BT_ERR_INVALID_ARGUMENT, "null context");
+    if (rank) *rank = c->impl.rank;
+    if (nranks) *nranks = c->impl.nranks;
+  });
+}
+
+int bt_ctx_stream(bt_ctx* c, void** stream) {
+  return guard([&] {
+    BT_REQUIRE(c && stream, BT_ERR_INVALID_ARGUMENT, "null argument");
+    *stream = c->impl.stream;
+  });
+}
+
+int bt_ctx_kernel_count(const bt_ctx* c, int64_t* count) {
+  return guard([&] {
+    BT_REQUIRE(c && count, BT_ERR_INVALID_ARGUMENT, "null argument");
+    *count = c->impl.kernels;
+  });
+}
+
+int bt_ctx_set_timing(bt_ctx* c, int on) {
+  return guard([&] {
+    BT_REQUIRE(c, BT_ERR_INVALID_ARGUMENT, "null context");
+    c->impl.timing = on != 0;
+  });
+}
+
+int bt_mat_create(bt_ctx* ctx, int64_t nbr, const int32_t* row_sizes, int64_t nbc,
+                  const int32_t* col_sizes, bt_mat** out) {
+  return guard([&] {
+    BT_REQUIRE(ctx && out, BT_ERR_INVALID_ARGUMENT, "null argument");
+    BT_REQUIRE(nbr >= 0 && nbc >= 0, BT_ERR_INVALID_ARGUMENT, "negative block count");
+    BT_REQUIRE(nbr < (int64_t(1) << 31) - 1 && nbc < (int64_t(1) << 31) - 1,
+               BT_ERR_INVALID_ARGUMENT, "block counts must fit int32");
+    BT_REQUIRE((nbr == 0 || row_sizes) && (nbc == 0 || col_sizes), BT_ERR_INVALID_ARGUMENT,
+               "null blocking");
+    for (int64_t t = 0; t < nbr; ++t)
+      BT_REQUIRE(row_sizes[t] >= 1, BT_ERR_INVALID_ARGUMENT,
+                 "Blocking: block sizes must be positive");
+    for (int64_t t = 0; t < nbc; ++t)
+      BT_REQUIRE(col_sizes[t] >= 1, BT_ERR_INVALID_ARGUMENT,
+                 "Blocking: block sizes must be positive");
+    BT_CUDA(cudaSetDevice(ctx->impl.device));
+    auto* m = new bt_mat;
+    Mat& x = m->impl;
+    x.ctx = &ctx->impl;
+    x.nbr = nbr;
+    x.nbc = nbc;
+    x.h_rsz.assign(row_sizes, row_sizes + nbr);
+    x.h_csz.assign(col_sizes, col_sizes + nbc);
+    upload_sizes(x);
+    x.init_empty();
+    *out = m;
+  });
+}
+
+int bt_mat_destroy(bt_mat* m) {
+  return guard([&] {
+    if (!m) return;
+    cudaSetDevice(m->impl.ctx->device);
+    delete m;
+  });
+}
+
+int bt_mat_clear(bt_mat* m) {
+  return guard([&] {
+    check_mat(m);
+    m->impl.init_empty();
+  });
+}
+
+int bt_mat_info(const bt_mat* m, int64_t* nblk, int64_t* nelems) {
+  return guard([&] {
+    check_mat(m);
+    if (nblk) *nblk = m->impl.nblk;
+    if (nelems) *nelems = m->impl.nelems;
+  });
+}
+
+int bt_mat_copy(const bt_mat* src, bt_mat* dst) {
+  return guard([&] {
+    check_mat(src);
+    check_mat(dst);
+    const Mat& s = src->impl;
+    Mat& d = dst->impl;
+    BT_REQUIRE(s.h_rsz == d.h_rsz && s.h_csz == d.h_csz, BT_ERR_INVALID_ARGUMENT,
+               "bt_mat_copy: blockings differ");
+    cudaStream_t st = d.stream();
+    if (s.stream() != st) BT_CUDA(cudaStreamSynchronize(s.stream()));
+    d.row_ptr.alloc(d.nbr + 1, st);
+    BT_CUDA(cudaMemcpyAsync(d.row_ptr.p, s.row_ptr.p, sizeof(int32_t) * (d.nbr + 1),
+                            cudaMemcpyDeviceToDevice, st));
+    d.col.alloc(std::max<int64_t>(s.nblk, 1), st);
+    d.off.alloc(std::max<int64_t>(s.nblk, 1), st);
+    d.vals.alloc(std::max<int64_t>(s.nvals, 2), st);
+    if (s.nblk) {
+      BT_CUDA(cudaMemcpyAsync(d.col.p, s.col.p, sizeof(int32_t) * s.nblk,
+                              cudaMemcpyDeviceToDevice, st));
+      BT_CUDA(cudaMemcpyAsync(d.off.p, s.off.p, sizeof(int64_t) * s.nblk,
+                              cudaMemcpyDeviceToDevice, st));
+      BT_CUDA(cudaMemcpyAsync(d.vals.p, s.vals.p, sizeof(double) * s.nvals,
+                              cudaMemcpyDeviceToDevice, st));
+    }
+    d.nblk = s.nblk;
+    d.nvals = s.nvals;
+    d.nelems = s.nelems;
+  });
+}
+
+int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* bj,
+                      const double* vals, int accumulate) {
+  return guard([&] {
+    check_mat(mh);
+    Mat& m = mh->impl;
+    BT_REQUIRE(n >= 0, BT_ERR_INVALID_ARGUMENT, "negative block count");
+    if (n == 0) return;
+    BT_REQUIRE(bi && bj && vals, BT_ERR_INVALID_ARGUMENT, "null input arrays");
+    cudaStream_t st = m.stream();
+    BT_CUDA(cudaSetDevice(m.ctx->device));
+    // validate + compact input offsets
+    std::vector<int64_t> in_off(n);
+    int64_t in_total = 0;
+    for (int64_t t = 0; t < n; ++t) {
+      BT_REQUIRE(bi[t] >= 0 && bi[t] < m.nbr && bj[t] >= 0 && bj[t] < m.nbc,
+                 BT_ERR_INVALID_ARGUMENT,
+                 "put_block: block (" + std::to_string(bi[t]) + "," + std::to_string(bj[t]) +
+                     ") out of range");
+      in_off[t] = in_total;
+      in_total += int64_t(m.h_rsz[bi[t]]) * m.h_csz[bj[t]];
+    }
+    // stable order of the batch by (i, j)
+    std::vector<int64_t> perm(n);
+    std::iota(perm.begin(), perm.end(), 0);
+    bool sorted = true;
+    for (int64_t t = 1; t < n && sorted; ++t)
+      if (bi[t] < bi[t - 1] || (bi[t] == bi[t - 1] && bj[t] < bj[t - 1])) sorted = false;
+    if (!sorted)
+      std::stable_sort(perm.begin(), perm.end(), [&](int64_t x, int64_t y) {
+        return bi[x] != bi[y] ? bi[x] < bi[y] : bj[x] < bj[y];
+      });
+    HostIndex old = download_index(m);
+    // merge old pattern with batch keys
+    std::vector<int32_t> row_ptr(m.nbr + 1, 0), col;
+    std::vector<int64_t> off, len, old_off, inp_ptr{0}, inp_src;
+    col.reserve(m.nblk + n);
+    int64_t nv = 0, ne = 0;
+    int64_t p = 0;
+    for (int64_t i = 0; i < m.nbr; ++i) {
+      int64_t e = old.row_ptr[i], e_end = old.row_ptr[i + 1];
+      while (e < e_end || (p < n && bi[perm[p]] == i)) {
+        int64_t j;
+        const bool have_old = e < e_end;
+        const bool have_new = p < n && bi[perm[p]] == i;
+        if (have_old && (!have_new || old.col[e] <= bj[perm[p]]))
+          j = old.col[e];
+        else
+          j = bj[perm[p]];
+        int64_t src_old = -1;
+        if (have_old && old.col[e] == j) {
+          src_old = old.off[e];
+          ++e;
+        }
+        // inputs with this key, in batch order
+        int64_t q = p;
+        while (q < n && bi[perm[q]] == i && bj[perm[q]] == j) ++q;
+        if (q > p) {
+          if (accumulate) {
+            for (int64_t t = p; t < q; ++t) inp_src.push_back(in_off[perm[t]]);
+          } else {
+            src_old = -1;  // replaced: the last input of the batch wins
+            inp_src.push_back(in_off[perm[q - 1]]);
+          }
+        }
+        p = q;
+        const int64_t L = int64_t(m.h_rsz[i]) * m.h_csz[j];
+        col.push_back(static_cast<int32_t>(j));
+        off.push_back(nv);
+        len.push_back(L);
+        old_off.push_back(src_old);
+        inp_ptr.push_back(static_cast<int64_t>(inp_src.size()));
+        nv += pad2(L);
+        ne += L;
+        row_ptr[i + 1]++;
+      }
+    }
+    for (int64_t i = 0; i < m.nbr; ++i) row_ptr[i + 1] += row_ptr[i];
+    BT_REQUIRE(col.size() < (size_t(1) << 31), BT_ERR_INVALID_ARGUMENT,
+               "store exceeds 2^31 blocks");
+    // device: stage inputs, build new slab
+    DBuf<double> d_in(in_total, st);
+    BT_CUDA(cudaMemcpyAsync(d_in.p, vals, sizeof(double) * in_total, cudaMemcpyHostToDevice, st));
+    const int64_t nout = static_cast<int64_t>(col.size());
+    DBuf<double> new_vals(std::max<int64_t>(nv, 2), st);
+    auto d_off = upload(off, st);
+    auto d_len = upload(len, st);
+    auto d_old = upload(old_off, st);
+    auto d_iptr = upload(inp_ptr, st);
+    auto d_isrc = upload(inp_src, st);
+    k_apply_put<<<static_cast<unsigned>(nout), 128, 0, st>>>(
+        new_vals.p, d_off.p, d_len.p, m.vals.p, d_old.p, d_in.p, d_iptr.p, d_isrc.p, nout);
+    check_launch("apply_put");
+    count_launch(m.ctx);
+    m.vals = std::move(new_vals);
+    install_pattern(m, row_ptr, col, off, nv, ne);
+    BT_CUDA(cudaStreamSynchronize(st));  // host buffers are borrowed for the call only
+  });
+}
+
+int bt_mat_export(const bt_mat* mh, int64_t* bi, int64_t* bj, double* vals) {
+  return guard([&] {
+    check_mat(mh);
+    const Mat& m = mh->impl;
+    BT_CUDA(cudaSetDevice(m.ctx->device));
+    if (m.nblk == 0) return;
+    cudaStream_t st = m.stream();
+    HostIndex h = download_index(m);
+    std::vector<int64_t> coff(m.nblk), len(m.nblk);
+    int64_t c = 0;
+    for (int64_t i = 0; i < m.nbr; ++i)
+      for (int32_t e = h.row_ptr[i]; e < h.row_ptr[i + 1]; ++e) {
+        if (bi) bi[e] = i;
+        if (bj) bj[e] = h.col[e];
+        len[e] = int64_t(m.h_rsz[i]) * m.h_csz[h.col[e]];
+        coff[e] = c;
+        c += len[e];
+      }
+    if (!vals) return;
+    DBuf<double> comp(std::max<int64_t>(c, 1), st);
+    auto d_coff = upload(coff, st);
+    auto d_len = upload(len, st);
+    const unsigned grid = static_cast<unsigned>((m.nblk * 32 + 255) / 256);
+    k_compact<<<grid, 256, 0, st>>>(comp.p, d_coff.p, m.vals.p, m.off.p, d_len.p, m.nblk);
+    check_launch("compact");
+    count_launch(m.ctx);
+    BT_CUDA(cudaMemcpyAsync(vals, comp.p, sizeof(double) * c, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int bt_mat_get_block(const bt_mat* mh, int64_t i, int64_t j, double* out, int* found) {
+  return guard([&] {
+    check_mat(mh);
+    const Mat& m = mh->impl;
+    BT_REQUIRE(found, BT_ERR_INVALID_ARGUMENT, "null found flag");
+    BT_REQUIRE(i >= 0 && i < m.nbr && j >= 0 && j < m.nbc, BT_ERR_INVALID_ARGUMENT,
+               "get_block: index out of range");
+    *found = 0;
+    if (m.nblk == 0) return;
+    cudaStream_t st = m.stream();
+    int32_t rp[2];
+    BT_CUDA(cudaMemcpyAsync(rp, m.row_ptr.p + i, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaStreamSynchronize(st));
+    if (rp[1] == rp[0]) return;
+    std::vector<int32_t> cols(rp[1] - rp[0]);
+    BT_CUDA(cudaMemcpyAsync(cols.data(), m.col.p + rp[0], sizeof(int32_t) * cols.size(),
+                            cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaStreamSynchronize(st));
+    auto it = std::lower_bound(cols.begin(), cols.end(), static_cast<int32_t>(j));
+    if (it == cols.end() || *it != j) return;
+    const int64_t e = rp[0] + (it - cols.begin());
+    int64_t o;
+    BT_CUDA(cudaMemcpyAsync(&o, m.off.p + e, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaStreamSynchronize(st));
+    if (out)
+      BT_CUDA(cudaMemcpyAsync(out, m.vals.p + o, sizeof(double) * m.h_rsz[i] * m.h_csz[j],
+                              cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaStreamSynchronize(st));
+    *found = 1;
+  });
+}
+
+int bt_mat_norms(const bt_mat* mh, double* out) {
+  return guard([&] {
+    check_mat(mh);
+    const Mat& m = mh->impl;
+    BT_REQUIRE(out || m.nblk == 0, BT_ERR_INVALID_ARGUMENT, "null output");
+    if (m.nblk == 0) return;
+    cudaStream_t st = m.stream();
+    DBuf<double> d(m.nblk, st);
+    k_block_norms<<<static_cast<unsigned>((m.nblk + 127) / 128), 128, 0, st>>>(
+        m.vals.p, m.row_ptr.p, m.col.p, m.off.p, m.rsz.p, m.csz.p, m.nbr, d.p, m.nblk);
+    check_launch("block_norms");
+    count_launch(m.ctx);
+    BT_CUDA(cudaMemcpyAsync(out, d.p, sizeof(double) * m.nblk, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int bt_filter(bt_mat* mh, double eps) {
+  return guard([&] {
+    check_mat(mh);
+    Mat& m = mh->impl;
+    if (m.nblk == 0 || !(eps > 0)) return;
+    cudaStream_t st = m.stream();
+    std::vector<double> nrm(m.nblk);
+    DBuf<double> d(m.nblk, st);
+    k_block_norms<<<static_cast<unsigned>((m.nblk + 127) / 128), 128, 0, st>>>(
+        m.vals.p, m.row_ptr.p, m.col.p, m.off.p, m.rsz.p, m.csz.p, m.nbr, d.p, m.nblk);
+    check_launch("block_norms");
+    count_launch(m.ctx);
+    BT_CUDA(cudaMemcpyAsync(nrm.data(), d.p, sizeof(double) * m.nblk, cudaMemcpyDeviceToHost, st));
+    HostIndex h = download_index(m);
+    std::vector<int32_t> row_ptr(m.nbr + 1, 0), col;
+    std::vector<int64_t> off, src, len;
+    int64_t nv = 0, ne = 0;
+    for (int64_t i = 0; i < m.nbr; ++i)
+      for (int32_t e = h.row_ptr[i]; e < h.row_ptr[i + 1]; ++e) {
+        if (nrm[e] < eps) continue;
+        const int64_t L = int64_t(m.h_rsz[i]) * m.h_csz[h.col[e]];
+        col.push_back(h.col[e]);
+        off.push_back(nv);
+        src.push_back(h.off[e]);
+        len.push_back(L);
+        nv += pad2(L);
+        ne += L;
+        row_ptr[i + 1]++;
+      }
+    for (int64_t i = 0; i < m.nbr; ++i) row_ptr[i + 1] += row_ptr[i];
+    const int64_t nout = static_cast<int64_t>(col.size());
+    DBuf<double> nvals(std::max<int64_t>(nv, 2), st);
+    if (nout) {
+      auto d_off = upload(off, st);
+      auto d_src = upload(src, st);
+      auto d_len = upload(len, st);
+      k_gather_blocks<<<static_cast<unsigned>((nout * 32 + 255) / 256), 256, 0, st>>>(
+          nvals.p, d_off.p, m.vals.p, d_src.p, d_len.p, nout);
+      check_launch("gather_blocks");
+      count_launch(m.ctx);
+    }
+    m.vals = std::move(nvals);
+    install_pattern(m, row_ptr, col, off, nv, ne);
+    BT_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+"""GPU parity: libbtcuda (through the C-ABI) vs the oracle on seeded inputs.
+
+Pattern and block index bit-exact; values within 1e-12 Frobenius-relative
+(north_star tolerance, FP64), globally and per block.
+"""
+import numpy as np
+import pytest
+
+from helpers import assert_parity, from_store, to_store
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(oracle, seed, rsz, ksz, nsz, occ_a, occ_b, occ_c, scale=0.0):
+    A = oracle.random_matrix(seed, rsz, ksz, occ_a, scale)
+    B = oracle.random_matrix(seed + 1, ksz, nsz, occ_b, scale)
+    Cin = oracle.random_matrix(seed + 2, rsz, nsz, occ_c, scale)
+    return A, B, Cin
+
+
+@pytest.mark.parametrize("bs", [1, 4, 5, 7, 8, 13, 16, 20, 23, 24, 32])
+def test_uniform_blocks(oracle, ctx, bs):
+    n = 12
+    A, B, Cin = _case(oracle, 100 + bs, [bs] * n, [bs] * n, [bs] * n, 0.3, 0.3, 0.1)
+    want, nprod, flops = oracle.multiply(A, B, Cin)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    from paper_1910_13555_b200.store import multiply_local
+    st = multiply_local(ctx, a, b, c)
+    assert st["products"] == nprod
+    assert st["flops"] == flops
+    assert_parity(from_store(c), want)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_mixed_blocks(oracle, ctx, seed):
+    rng = np.random.default_rng(seed)
+    rsz = rng.integers(1, 10, 9).astype(np.int32)
+    ksz = rng.integers(1, 10, 7).astype(np.int32)
+    nsz = rng.integers(1, 10, 8).astype(np.int32)
+    A, B, Cin = _case(oracle, 10 * seed, rsz, ksz, nsz, 0.4, 0.4, 0.2)
+    want, nprod, _ = oracle.multiply(A, B, Cin)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    from paper_1910_13555_b200.store import multiply_local
+    st = multiply_local(ctx, a, b, c)
+    assert st["products"] == nprod
+    assert_parity(from_store(c), want)
+
+
+def test_h2o_sizes_with_filter(oracle, ctx):
+    rng = np.random.default_rng(5)
+    sizes = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 40)]
+    A, B, Cin = _case(oracle, 77, sizes, sizes, sizes, 0.2, 0.2, 0.0, scale=12.0)
+    for eps in (0.0, 1e-8):
+        want, nprod, flops = oracle.multiply(A, B, Cin, eps)
+        a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+        from paper_1910_13555_b200.store import multiply_local
+        st = multiply_local(ctx, a, b, c, eps)
+        assert st["products"] == nprod
+        assert st["flops"] == flops
+        assert_parity(from_store(c), want)
+
+
+def test_tall_blocks(oracle, ctx):
+    rsz = np.array([169, 299, 529, 40], np.int32)
+    ksz = np.array([13, 23, 13, 23, 13], np.int32)
+    nsz = np.array([23, 13, 23], np.int32)
+    A, B, Cin = _case(oracle, 5, rsz, ksz, nsz, 0.6, 0.6, 0.3)
+    want, nprod, _ = oracle.multiply(A, B, Cin)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    from paper_1910_13555_b200.store import multiply_local
+    multiply_local(ctx, a, b, c)
+    assert_parity(from_store(c), want)
+
+
+def test_generic_large_blocks(oracle, ctx):
+    A, B, Cin = _case(oracle, 9, [40, 70], [33, 80, 20], [48, 65], 0.8, 0.8, 0.5)
+    want, _, _ = oracle.multiply(A, B, Cin)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    from paper_1910_13555_b200.store import multiply_local
+    multiply_local(ctx, a, b, c)
+    assert_parity(from_store(c), want)
+
+
+def test_config1_pattern_and_values(oracle, ctx):
+    """BASELINE config 1 (400^2 blocks of 23, 10 %), pinned seeds 1001/1002."""
+    sz = np.full(400, 23, np.int32)
+    A = oracle.random_matrix(1001, sz, sz, 0.10)
+    B = oracle.random_matrix(1002, sz, sz, 0.10)
+    Cin = oracle.random_matrix(1003, sz, sz, 0.0)
+    want, nprod, flops = oracle.multiply(A, B, Cin)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    from paper_1910_13555_b200.store import multiply_local
+    st = multiply_local(ctx, a, b, c)
+    assert st["products"] == nprod and st["flops"] == flops
+    assert_parity(from_store(c), want)
