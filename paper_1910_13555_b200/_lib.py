@@ -102,7 +102,7 @@ def load(path: str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("BT_LIB") or LIB_PATH
     if not os.path.exists(p):
         raise ImportError(f"{p} not built: run `make -C paper_1910_13555_b200/csrc` "
                           "(or __graft_entry__.build())")

@@ -111,10 +111,14 @@ struct Ctx {
 // One rank's block-CSR store, device resident:
 //   row_ptr[nbr+1] int32 over ALL block rows (dense row pointer),
 //   col[nblk]      int32 global block column, strictly increasing per row,
-//   off[nblk]      int64 element offset of the block in vals; every block slot is
-//                  padded to an even element count so each starts 16-byte aligned
-//                  (cp.async.bulk / vector access),
-//   vals           padded FP64 slab, row-major m x n blocks.
+//   off[nblk]      int64 offset (in doubles, a multiple of 64) of the block in vals,
+//   vals           FP64 slab of blocks in the "T8" layout: each m x n block is
+//                  zero-padded to ceil8(m) x ceil8(n) and stored as row-major 8x8
+//                  tiles of 64 doubles (512 B), element (r, c) of a tile at
+//                  r*8 + (c ^ 4*((r>>1)&1)).  The swizzle makes DMMA A-role
+//                  (8x4) and B-role (4x8) fragment reads and the C fragment
+//                  16-byte stores bank-conflict free; tile rows are contiguous,
+//                  so a 32-row slab of a tall block is one bulk copy.
 struct Mat {
   Ctx* ctx = nullptr;
   int64_t nbr = 0, nbc = 0;
@@ -134,6 +138,18 @@ struct Mat {
 };
 
 __host__ __device__ inline int64_t pad2(int64_t x) { return (x + 1) & ~int64_t(1); }
+
+// ---- T8 block layout helpers
+__host__ __device__ inline int tiles8(int x) { return (x + 7) >> 3; }
+// doubles occupied by an m x n block
+__host__ __device__ inline int64_t t8_size(int m, int n) {
+  return static_cast<int64_t>(tiles8(m)) * tiles8(n) * 64;
+}
+// position of element (r, c) inside a T8 block with `ntc` tile columns
+__host__ __device__ inline int64_t t8_pos(int r, int c, int ntc) {
+  return ((static_cast<int64_t>(r >> 3) * ntc + (c >> 3)) << 6) + ((r & 7) << 3) +
+         ((c & 7) ^ (((r >> 1) & 1) << 2));
+}
 
 // launch accounting
 inline void count_launch(Ctx* c, int n = 1) { c->kernels += n; }

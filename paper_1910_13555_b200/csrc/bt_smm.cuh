@@ -1,0 +1,291 @@
+// bt_smm.cuh -- the libsmm_acc-equivalent small-GEMM family for sm_100a (FP64).
+//
+// Reference op: block_gemm_acc (block.hpp:45-60), c += a*b over a batch ordered
+// by (row, col, k) (order_batches, block.hpp:112-118).
+//
+// Data path:
+//  * Operands live in the native T8 layout (bt_internal.cuh): zero-padded 8x8
+//    swizzled tiles, so A-role (8x4) and B-role (4x8) fragment reads from
+//    shared memory are bank-conflict free and need no k-masking, and C tiles
+//    are read/written as coalesced 16-byte pairs.
+//  * Each product is a (A slab, B block) pair moved by the bulk-async copy engine
+//    (cp.async.bulk, TMA 1D) into a per-warp ring of shared-memory stages that
+//    complete on mbarriers; the producer runs `stages` products ahead.
+//  * One warp owns one C tile (<= 32 x 32) for its whole product chain: the
+//    accumulators stay in registers, C is read (C_in) and written exactly once.
+//  * Warps pull C tiles from a global atomic counter over an L2-friendly band
+//    order.
+#pragma once
+
+#include "bt_internal.cuh"
+#include "bt_ptx.cuh"
+
+namespace bt {
+
+// One C tile of work: rows [r0, r0 + rows) of C block (i, j).  32 bytes.
+struct Item {
+  int64_t c_off;    // element offset of the tile's first row in the C_out slab
+  int64_t cin_off;  // same for C_in, or -1
+  int64_t p0r8;     // first product (low 48 bits) | (r0 / 8) << 48
+  int32_t np;       // number of products
+  int16_t rows;     // rows in this tile (<= TM)
+  int16_t n;        // C block columns (row stride)
+};
+
+// Product descriptor: offsets of the A and B blocks in units of one 8x8 tile
+// (64 doubles) and the number of 4-wide k chunks.
+using Desc = int4;  // {a_unit, b_unit, kc, 0}
+
+struct NumArgs {
+  const Item* items;
+  int64_t item_lo;
+  int64_t nitems;
+  unsigned long long* counter;
+  const Desc* desc;
+  const double* at;  // A values (T8)
+  const double* bt;  // B values (T8)
+  const double* cin;
+  double* cout;
+  int stages;
+  int stage_doubles;  // per-stage shared memory in doubles
+  int a_region;       // doubles of the A part of a stage
+};
+
+__device__ __forceinline__ int64_t item_p0(const Item& it) {
+  return it.p0r8 & ((int64_t(1) << 48) - 1);
+}
+__device__ __forceinline__ int item_r8(const Item& it) {
+  return static_cast<int>(it.p0r8 >> 48);
+}
+
+// FP64 DMMA tile kernel: warp <-> C tile of up to TM = 8*TMT rows and exactly
+// TN = 8*TNT padded columns.
+//
+// Warps take tickets for items of the band-ordered list from a global counter,
+// so the warps running at any moment sit on neighbouring C tiles (shared A band
+// in L2) and finish together.  Producer side (issue of bulk copies) runs
+// `stages` products ahead of the consumer; tickets are drawn three items ahead,
+// item structs loaded two ahead and product descriptors one ahead (one
+// coalesced load, distributed by shuffles), so no dependent global load sits on
+// the DMMA critical path.
+#ifndef BT_DMMA_MINBLOCKS
+#define BT_DMMA_MINBLOCKS 1
+#endif
+template <int TMT, int TNT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, BT_DMMA_MINBLOCKS) k_smm_dmma(const NumArgs g) {
+  constexpr int QN = 8;  // per-warp queue of items between producer and consumer
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int S = g.stages;
+  // per-lane T8 positions of the DMMA fragments (bt_internal.cuh layout)
+  const int sw_g = ((gq >> 1) & 1) << 2;
+  const int la0 = gq * 8 + (tq ^ sw_g), la1 = gq * 8 + ((4 + tq) ^ sw_g);  // A (g, 4h+t)
+  const int swt = ((tq >> 1) & 1) << 2;
+  const int lb0 = tq * 8 + (gq ^ swt), lb1 = (4 + tq) * 8 + (gq ^ swt);    // B (4h+t, g)
+  const int lc = gq * 8 + ((2 * tq) ^ sw_g);                               // C (g, 2t..2t+1)
+  // per-warp control block (512 B): 8 mbarriers | 8 stage kc | QN items
+  unsigned char* ctl = smem + wid * 512;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ctl);
+  int* stage_kc = reinterpret_cast<int*>(ctl + 64);
+  Item* q_items = reinterpret_cast<Item*>(ctl + 256);
+  double* stages = reinterpret_cast<double*>(smem + WARPS * 512) +
+                   static_cast<int64_t>(wid) * S * g.stage_doubles;
+
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const Item* items = g.items + g.item_lo;
+  // Item pipeline (dynamic work distribution, three deep so that no atomic or
+  // dependent load result is consumed in the step that issued it):
+  //   id3: ticket from the global counter (atomic in flight)
+  //   n2 : item struct loading (id known)
+  //   n1 : struct ready, its product descriptors loading (one per lane)
+  auto ticket = [&]() -> int64_t {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(g.counter, 1ull);
+    return static_cast<int64_t>(__shfl_sync(0xffffffffu, v, 0));
+  };
+  int64_t idx_n1 = ticket();
+  int64_t idx_n2 = ticket();
+  int64_t id3 = ticket();
+  Item n1{}, n2{};
+  Desc n1_desc = make_int4(0, 0, 0, 0);
+  if (idx_n1 < g.nitems) n1 = items[idx_n1];
+  if (idx_n2 < g.nitems) n2 = items[idx_n2];
+  if (idx_n1 < g.nitems && lane < n1.np) n1_desc = g.desc[item_p0(n1) + lane];
+
+  uint32_t issued = 0, consumed = 0;
+  int qh = 0, qt = 0;
+  // producer's current item
+  int64_t p_pos = 0, p_end = 0, d_base = 0;
+  int p_r8 = 0, p_mt = 0;
+  Desc p_desc = make_int4(0, 0, 0, 0);
+  bool p_more = true;
+
+  auto top_up = [&]() {
+    while (issued - consumed < static_cast<uint32_t>(S)) {
+      if (p_pos >= p_end) {
+        if (!p_more || qt - qh >= QN) return;
+        if (idx_n1 >= g.nitems) {
+          p_more = false;
+          return;
+        }
+        // advance: current <- n1, n1 <- n2 (+ its descs), n2 <- next struct
+        if (lane == 0) q_items[qt % QN] = n1;
+        ++qt;
+        p_pos = item_p0(n1);
+        p_end = p_pos + n1.np;
+        d_base = p_pos;
+        p_r8 = item_r8(n1);
+        p_mt = (n1.rows + 7) >> 3;
+        p_desc = n1_desc;
+        idx_n1 = idx_n2;
+        n1 = n2;
+        n1_desc = make_int4(0, 0, 0, 0);
+        if (idx_n1 < g.nitems && lane < n1.np) n1_desc = g.desc[item_p0(n1) + lane];
+        idx_n2 = id3;
+        if (idx_n2 < g.nitems) n2 = items[idx_n2];
+        id3 = idx_n2 < g.nitems ? ticket() : g.nitems;
+        continue;
+      }
+      if (p_pos - d_base >= 32) {  // items with more than 32 products
+        d_base = p_pos;
+        p_desc = lane < p_end - p_pos ? g.desc[p_pos + lane] : make_int4(0, 0, 0, 0);
+      }
+      const int src = static_cast<int>(p_pos - d_base);
+      Desc d;
+      d.x = __shfl_sync(0xffffffffu, p_desc.x, src);
+      d.y = __shfl_sync(0xffffffffu, p_desc.y, src);
+      d.z = __shfl_sync(0xffffffffu, p_desc.z, src);
+      const int s = static_cast<int>(issued % static_cast<uint32_t>(S));
+      if (lane == 0) {
+        const int KT = (d.z + 1) >> 1;  // 8-wide k tiles
+        const uint32_t ba = static_cast<uint32_t>(p_mt * KT) * 512u;
+        const uint32_t bb = static_cast<uint32_t>(KT * TNT) * 512u;
+        double* st = stages + static_cast<int64_t>(s) * g.stage_doubles;
+        stage_kc[s] = d.z;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[s], ba + bb);
+        bulk_g2s(st, g.at + (static_cast<int64_t>(d.x) + static_cast<int64_t>(p_r8) * KT) * 64,
+                 ba, &bars[s]);
+        bulk_g2s(st + g.a_region, g.bt + static_cast<int64_t>(d.y) * 64, bb, &bars[s]);
+      }
+      ++issued;
+      ++p_pos;
+    }
+  };
+
+  top_up();
+  __syncwarp();
+  while (qh < qt) {
+    const Item it = q_items[qh % QN];
+    const int mt = (it.rows + 7) >> 3;  // 8-row tiles present in this C tile
+    double acc[TMT][TNT][2];
+#pragma unroll
+    for (int tm = 0; tm < TMT; ++tm)
+#pragma unroll
+      for (int tn = 0; tn < TNT; ++tn) {
+        acc[tm][tn][0] = 0.0;
+        acc[tm][tn][1] = 0.0;
+      }
+    if (it.cin_off >= 0) {
+#pragma unroll
+      for (int tm = 0; tm < TMT; ++tm)
+        if (tm < mt) {
+#pragma unroll
+          for (int tn = 0; tn < TNT; ++tn) {
+            const double2 v = *reinterpret_cast<const double2*>(
+                g.cin + it.cin_off + ((tm * TNT + tn) << 6) + lc);
+            acc[tm][tn][0] = v.x;
+            acc[tm][tn][1] = v.y;
+          }
+        }
+    }
+    for (int t = 0; t < it.np; ++t) {
+      const int s = static_cast<int>(consumed % static_cast<uint32_t>(S));
+      mbar_wait(&bars[s], (consumed / static_cast<uint32_t>(S)) & 1u);
+      const int kc = stage_kc[s];
+      const int KT = (kc + 1) >> 1;
+      const double* sA = stages + static_cast<int64_t>(s) * g.stage_doubles;
+      const double* sB = sA + g.a_region;
+      // k tiles, unrolled by 4 with uniform guards (KT <= 8 for DMMA classes)
+      for (int kt0 = 0; kt0 < KT; kt0 += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kt = kt0 + u;
+          if (kt < KT) {
+            // two 4-wide k chunks per 8x8 tile column (the second may be padding)
+            double af[2][TMT], bf[2][TNT];
+#pragma unroll
+            for (int tm = 0; tm < TMT; ++tm) {
+              af[0][tm] = sA[((tm * KT + kt) << 6) + la0];
+              af[1][tm] = sA[((tm * KT + kt) << 6) + la1];
+            }
+#pragma unroll
+            for (int tn = 0; tn < TNT; ++tn) {
+              bf[0][tn] = sB[((kt * TNT + tn) << 6) + lb0];
+              bf[1][tn] = sB[((kt * TNT + tn) << 6) + lb1];
+            }
+#pragma unroll
+            for (int tm = 0; tm < TMT; ++tm)
+#pragma unroll
+              for (int tn = 0; tn < TNT; ++tn)
+                dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[0][tm], bf[0][tn]);
+            if (2 * kt + 1 < kc) {
+#pragma unroll
+              for (int tm = 0; tm < TMT; ++tm)
+#pragma unroll
+                for (int tn = 0; tn < TNT; ++tn)
+                  dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[1][tm], bf[1][tn]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      ++consumed;
+      top_up();
+    }
+    double* dst = g.cout + it.c_off;
+#pragma unroll
+    for (int tm = 0; tm < TMT; ++tm)
+      if (tm < mt) {
+#pragma unroll
+        for (int tn = 0; tn < TNT; ++tn)
+          __stcs(reinterpret_cast<double2*>(dst + ((tm * TNT + tn) << 6) + lc),
+                 make_double2(acc[tm][tn][0], acc[tm][tn][1]));
+      }
+    ++qh;
+    top_up();
+    __syncwarp();
+  }
+}
+
+// Generic small-GEMM (n > 32 or k > 64): one CTA per C block, one thread per
+// element, T8 operands, products in k order.
+__global__ void k_smm_generic(const NumArgs g) {
+  const int64_t id = g.item_lo + blockIdx.x;
+  if (blockIdx.x >= g.nitems) return;
+  const Item it = g.items[id];
+  const int m = it.rows, n = it.n;
+  const int NT = tiles8(n);
+  const int64_t p0 = item_p0(it);
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int r = e / n, q = e - r * n;
+    const int64_t cp = t8_pos(r, q, NT);
+    double acc = it.cin_off >= 0 ? g.cin[it.cin_off + cp] : 0.0;
+    for (int p = 0; p < it.np; ++p) {
+      const Desc d = g.desc[p0 + p];
+      const int KT = (d.z + 1) >> 1;
+      const double* a = g.at + static_cast<int64_t>(d.x) * 64;
+      const double* b = g.bt + static_cast<int64_t>(d.y) * 64;
+      for (int c = 0; c < 4 * d.z; ++c) acc = fma(a[t8_pos(r, c, KT)], b[t8_pos(c, q, NT)], acc);
+    }
+    g.cout[it.c_off + cp] = acc;
+  }
+}
+
+}  // namespace bt

@@ -70,49 +70,54 @@ __global__ void k_gather_blocks(double* __restrict__ dst, const int64_t* __restr
   if (so < 0) return;
   const double2* s = reinterpret_cast<const double2*>(src + so);
   double2* d = reinterpret_cast<double2*>(dst + dst_off[w]);
-  const int64_t n2 = pad2(len[w]) >> 1;
+  const int64_t n2 = len[w] >> 1;  // T8 slots: multiples of 64 doubles
   for (int64_t t = lane; t < n2; t += 32) d[t] = s[t];
 }
 
 // Put plan application: output block w = base (old slot or first input) +
 // remaining inputs in batch order (LocalStore::insert accumulate semantics,
-// matrix.hpp:176-179).
+// matrix.hpp:176-179).  Inputs are compact row-major, old/new slots are T8;
+// the new slab is zeroed beforehand so T8 padding stays zero.
 __global__ void k_apply_put(double* __restrict__ dst, const int64_t* __restrict__ dst_off,
-                            const int64_t* __restrict__ len, const double* __restrict__ old,
+                            const int2* __restrict__ dims, const double* __restrict__ old,
                             const int64_t* __restrict__ old_off,
                             const double* __restrict__ inp, const int64_t* __restrict__ inp_ptr,
                             const int64_t* __restrict__ inp_src, int64_t n) {
   const int64_t w = blockIdx.x;
   if (w >= n) return;
-  const int64_t L = len[w];
+  const int m = dims[w].x, nn = dims[w].y, ntc = tiles8(nn);
   double* d = dst + dst_off[w];
   const int64_t oo = old_off[w];
   const int64_t i0 = inp_ptr[w], i1 = inp_ptr[w + 1];
-  for (int64_t e = threadIdx.x; e < L; e += blockDim.x) {
+  for (int e = threadIdx.x; e < m * nn; e += blockDim.x) {
+    const int r = e / nn, c = e - r * nn;
+    const int64_t tp = t8_pos(r, c, ntc);
     double v;
     int64_t t = i0;
     if (oo >= 0) {
-      v = old[oo + e];
+      v = old[oo + tp];
     } else {
       v = inp[inp_src[t] + e];
       ++t;
     }
     for (; t < i1; ++t) v = __dadd_rn(v, inp[inp_src[t] + e]);
-    d[e] = v;
+    d[tp] = v;
   }
 }
 
-// padded slot -> compact host-order slot
+// T8 slot -> compact row-major (host order)
 __global__ void k_compact(double* __restrict__ dst, const int64_t* __restrict__ dst_off,
                           const double* __restrict__ src, const int64_t* __restrict__ src_off,
-                          const int64_t* __restrict__ len, int64_t n) {
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+                          const int2* __restrict__ dims, int64_t n) {
+  const int64_t w = blockIdx.x;
   if (w >= n) return;
+  const int m = dims[w].x, nn = dims[w].y, ntc = tiles8(nn);
   const double* s = src + src_off[w];
   double* d = dst + dst_off[w];
-  const int64_t L = len[w];
-  for (int64_t t = lane; t < L; t += 32) d[t] = s[t];
+  for (int e = threadIdx.x; e < m * nn; e += blockDim.x) {
+    const int r = e / nn, c = e - r * nn;
+    d[e] = s[t8_pos(r, c, ntc)];
+  }
 }
 
 // Frobenius norm per block: sequential sum of squares, unfused.
@@ -128,10 +133,14 @@ __global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __
     int64_t mid = (lo + hi) >> 1;
     if (row_ptr[mid] <= b) lo = mid; else hi = mid;
   }
-  const int64_t L = (int64_t)rsz[lo] * csz[col[b]];
+  const int m = rsz[lo], n = csz[col[b]], ntc = tiles8(n);
   const double* p = vals + off[b];
   double s = 0.0;
-  for (int64_t t = 0; t < L; ++t) s = __dadd_rn(s, __dmul_rn(p[t], p[t]));
+  for (int r = 0; r < m; ++r)  // row-major element order, as the reference stores it
+    for (int c = 0; c < n; ++c) {
+      const double v = p[t8_pos(r, c, ntc)];
+      s = __dadd_rn(s, __dmul_rn(v, v));
+    }
   out[b] = __dsqrt_rn(s);
 }
 
@@ -418,7 +427,8 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
     HostIndex old = download_index(m);
     // merge old pattern with batch keys
     std::vector<int32_t> row_ptr(m.nbr + 1, 0), col;
-    std::vector<int64_t> off, len, old_off, inp_ptr{0}, inp_src;
+    std::vector<int64_t> off, old_off, inp_ptr{0}, inp_src;
+    std::vector<int2> dims;
     col.reserve(m.nblk + n);
     int64_t nv = 0, ne = 0;
     int64_t p = 0;
@@ -452,10 +462,10 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
         const int64_t L = int64_t(m.h_rsz[i]) * m.h_csz[j];
         col.push_back(static_cast<int32_t>(j));
         off.push_back(nv);
-        len.push_back(L);
+        dims.push_back(make_int2(m.h_rsz[i], m.h_csz[j]));
         old_off.push_back(src_old);
         inp_ptr.push_back(static_cast<int64_t>(inp_src.size()));
-        nv += pad2(L);
+        nv += t8_size(m.h_rsz[i], m.h_csz[j]);
         ne += L;
         row_ptr[i + 1]++;
       }
@@ -468,13 +478,14 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
     BT_CUDA(cudaMemcpyAsync(d_in.p, vals, sizeof(double) * in_total, cudaMemcpyHostToDevice, st));
     const int64_t nout = static_cast<int64_t>(col.size());
     DBuf<double> new_vals(std::max<int64_t>(nv, 2), st);
+    BT_CUDA(cudaMemsetAsync(new_vals.p, 0, sizeof(double) * std::max<int64_t>(nv, 2), st));
     auto d_off = upload(off, st);
-    auto d_len = upload(len, st);
+    auto d_dims = upload(dims, st);
     auto d_old = upload(old_off, st);
     auto d_iptr = upload(inp_ptr, st);
     auto d_isrc = upload(inp_src, st);
     k_apply_put<<<static_cast<unsigned>(nout), 128, 0, st>>>(
-        new_vals.p, d_off.p, d_len.p, m.vals.p, d_old.p, d_in.p, d_iptr.p, d_isrc.p, nout);
+        new_vals.p, d_off.p, d_dims.p, m.vals.p, d_old.p, d_in.p, d_iptr.p, d_isrc.p, nout);
     check_launch("apply_put");
     count_launch(m.ctx);
     m.vals = std::move(new_vals);
@@ -491,22 +502,23 @@ int bt_mat_export(const bt_mat* mh, int64_t* bi, int64_t* bj, double* vals) {
     if (m.nblk == 0) return;
     cudaStream_t st = m.stream();
     HostIndex h = download_index(m);
-    std::vector<int64_t> coff(m.nblk), len(m.nblk);
+    std::vector<int64_t> coff(m.nblk);
+    std::vector<int2> dims(m.nblk);
     int64_t c = 0;
     for (int64_t i = 0; i < m.nbr; ++i)
       for (int32_t e = h.row_ptr[i]; e < h.row_ptr[i + 1]; ++e) {
         if (bi) bi[e] = i;
         if (bj) bj[e] = h.col[e];
-        len[e] = int64_t(m.h_rsz[i]) * m.h_csz[h.col[e]];
+        dims[e] = make_int2(m.h_rsz[i], m.h_csz[h.col[e]]);
         coff[e] = c;
-        c += len[e];
+        c += int64_t(dims[e].x) * dims[e].y;
       }
     if (!vals) return;
     DBuf<double> comp(std::max<int64_t>(c, 1), st);
     auto d_coff = upload(coff, st);
-    auto d_len = upload(len, st);
-    const unsigned grid = static_cast<unsigned>((m.nblk * 32 + 255) / 256);
-    k_compact<<<grid, 256, 0, st>>>(comp.p, d_coff.p, m.vals.p, m.off.p, d_len.p, m.nblk);
+    auto d_dims = upload(dims, st);
+    k_compact<<<static_cast<unsigned>(m.nblk), 128, 0, st>>>(comp.p, d_coff.p, m.vals.p, m.off.p,
+                                                             d_dims.p, m.nblk);
     check_launch("compact");
     count_launch(m.ctx);
     BT_CUDA(cudaMemcpyAsync(vals, comp.p, sizeof(double) * c, cudaMemcpyDeviceToHost, st));
@@ -538,10 +550,15 @@ int bt_mat_get_block(const bt_mat* mh, int64_t i, int64_t j, double* out, int* f
     int64_t o;
     BT_CUDA(cudaMemcpyAsync(&o, m.off.p + e, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     BT_CUDA(cudaStreamSynchronize(st));
-    if (out)
-      BT_CUDA(cudaMemcpyAsync(out, m.vals.p + o, sizeof(double) * m.h_rsz[i] * m.h_csz[j],
+    if (out) {
+      const int R = m.h_rsz[i], Cc = m.h_csz[j];
+      std::vector<double> slot(t8_size(R, Cc));
+      BT_CUDA(cudaMemcpyAsync(slot.data(), m.vals.p + o, sizeof(double) * slot.size(),
                               cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaStreamSynchronize(st));
+      BT_CUDA(cudaStreamSynchronize(st));
+      for (int r = 0; r < R; ++r)
+        for (int c = 0; c < Cc; ++c) out[int64_t(r) * Cc + c] = slot[t8_pos(r, c, tiles8(Cc))];
+    }
     *found = 1;
   });
 }
@@ -584,11 +601,12 @@ int bt_filter(bt_mat* mh, double eps) {
       for (int32_t e = h.row_ptr[i]; e < h.row_ptr[i + 1]; ++e) {
         if (nrm[e] < eps) continue;
         const int64_t L = int64_t(m.h_rsz[i]) * m.h_csz[h.col[e]];
+        const int64_t T = t8_size(m.h_rsz[i], m.h_csz[h.col[e]]);
         col.push_back(h.col[e]);
         off.push_back(nv);
         src.push_back(h.off[e]);
-        len.push_back(L);
-        nv += pad2(L);
+        len.push_back(T);
+        nv += T;
         ne += L;
         row_ptr[i + 1]++;
       }

@@ -15,6 +15,7 @@ A = o.random_matrix(1001, sz, sz, occ)
 B = o.random_matrix(1002, sz, sz, occ)
 print("gen", time.time() - t, A.nblk, B.nblk, flush=True)
 ctx = Context(0)
+ctx.set_timing(True)
 a = LocalStore(ctx, sz, sz); a.put_blocks(A.bi, A.bj, A.vals)
 b = LocalStore(ctx, sz, sz); b.put_blocks(B.bi, B.bj, B.vals)
 c = LocalStore(ctx, sz, sz)
@@ -24,4 +25,4 @@ for it in range(8):
     st = multiply_local(ctx, a, b, c)
     ctx.sync()
     dt = time.perf_counter() - t0
-    print(f"iter {it}: {dt*1e3:.3f} ms  {st['flops']/dt/1e9:.1f} GFLOP/s  products {st['products']} kernels {st['kernels']}", flush=True)
+    print(f"iter {it}: {dt*1e3:.3f} ms  {st['flops']/dt/1e9:.1f} GFLOP/s  numeric {st['ms_numeric']:.3f} ms = {st['flops']/st['ms_numeric']/1e9:.1f} GFLOP/s total-dev {st['ms_total']:.3f} ms  products {st['products']} kernels {st['kernels']}", flush=True)
