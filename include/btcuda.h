@@ -124,6 +124,51 @@ int bt_multiply(bt_ctx* ctx, const bt_mat* a, const bt_mat* b, bt_mat* c, double
 /* Post-filter: drops C blocks with ||C_ij||_F < eps. */
 int bt_filter(bt_mat* m, double eps);
 
+/* ------------------------------------------------------ distributed layer */
+typedef struct bt_grid bt_grid; /* process group + ledger: SimComm (comm.hpp:152-397) */
+typedef struct bt_dmat bt_dmat; /* DistMatrix (matrix.hpp:279-401) */
+
+/* A group of nranks ranks.  With a single-rank context all ranks are local
+ * "virtual ranks" on the context's GPU (messages are device copies): the
+ * reference's one-process SimComm.  With an NCCL context (bt_ctx_create with
+ * nranks > 1) the group is the NCCL world and this process owns rank ctx.rank. */
+int bt_grid_create(bt_ctx* ctx, int nranks, bt_grid** out);
+int bt_grid_destroy(bt_grid* g);
+int bt_grid_info(const bt_grid* g, int* nranks, int* first_local, int* nlocal);
+/* Ledger (comm.hpp:60-150): what = 0 elements sent, 1 elements received,
+ * 2 meta sent, 3 meta received; phase NULL/"" = rank total. */
+int bt_grid_ledger(const bt_grid* g, int rank, const char* phase, int what, int64_t* out);
+int bt_grid_reset_ledger(bt_grid* g);
+
+/* new_matrix (matrix.hpp:404-410): blockings + ProcessGrid dims + Axis
+ * distributions; NULL distributions = round robin (new_matrix_round_robin,
+ * matrix.hpp:413-418). */
+int bt_dmat_create(bt_grid* g, int64_t nbr, const int32_t* row_sizes, int64_t nbc,
+                   const int32_t* col_sizes, int grid_rows, int grid_cols,
+                   const int32_t* row_dist, const int32_t* col_dist, bt_dmat** out);
+int bt_dmat_destroy(bt_dmat* d);
+/* the store of a local rank (DistMatrix::local, matrix.hpp:294-295); borrowed */
+int bt_dmat_local(bt_dmat* d, int rank, bt_mat** store);
+/* DistMatrix::owner_rank (matrix.hpp:297-299) */
+int bt_dmat_owner(const bt_dmat* d, int64_t i, int64_t j, int* rank);
+/* put_block routed to the owner (matrix.hpp:305-309); BT_ERR_OWNERSHIP when the
+ * owner is a rank of another process */
+int bt_dmat_put_blocks(bt_dmat* d, int64_t n, const int64_t* bi, const int64_t* bj,
+                       const double* vals, int accumulate);
+/* redistribute / redistribute_add (matrix.hpp:567-622) onto dst's layout */
+int bt_redistribute(const bt_dmat* src, bt_dmat* dst, int transpose, int accumulate,
+                    const char* phase);
+/* multiply_cannon (multiply_cannon.hpp:62-118) */
+int bt_multiply_cannon(const bt_dmat* a, const bt_dmat* b, bt_dmat* c, double eps,
+                       bt_stats* stats);
+/* multiply_reduce_case1 (multiply_rect.hpp:123-192) */
+int bt_multiply_case1(const bt_dmat* a, const bt_dmat* b, bt_dmat* c, int nprocs, double eps,
+                      bt_stats* stats);
+/* multiply_virtual_case2 (multiply_rect.hpp:199-238); gather = 1 gathers all B
+ * slabs in one NVLink step instead of the P-step ring */
+int bt_multiply_case2(const bt_dmat* a, const bt_dmat* b, bt_dmat* c, int nprocs, int gather,
+                      double eps, bt_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,25 @@ SIGNATURES = {
     "bt_multiply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                               C.POINTER(BtStats)]),
     "bt_filter": (C.c_int, [C.c_void_p, C.c_double]),
+    "bt_grid_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "bt_grid_destroy": (C.c_int, [C.c_void_p]),
+    "bt_grid_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                               C.POINTER(C.c_int)]),
+    "bt_grid_ledger": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_int, _i64p]),
+    "bt_grid_reset_ledger": (C.c_int, [C.c_void_p]),
+    "bt_dmat_create": (C.c_int, [C.c_void_p, C.c_int64, _i32p, C.c_int64, _i32p, C.c_int,
+                                 C.c_int, _i32p, _i32p, C.POINTER(C.c_void_p)]),
+    "bt_dmat_destroy": (C.c_int, [C.c_void_p]),
+    "bt_dmat_local": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    "bt_dmat_owner": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_int)]),
+    "bt_dmat_put_blocks": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _f64p, C.c_int]),
+    "bt_redistribute": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_char_p]),
+    "bt_multiply_cannon": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                     C.POINTER(BtStats)]),
+    "bt_multiply_case1": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                    C.POINTER(BtStats)]),
+    "bt_multiply_case2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                    C.c_double, C.POINTER(BtStats)]),
 }
 
 _lib = None

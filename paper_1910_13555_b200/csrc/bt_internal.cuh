@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -105,6 +106,15 @@ struct Ctx {
   bool timing = false;          // record CUDA events around multiply kernels
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   void* ensure_scratch(size_t bytes);
+  // Grow-only per-slot workspace for call-local temporaries (no allocator calls
+  // in steady state).  Valid until the next use of the same slot.
+  DBuf<unsigned char> ws_slots[24];
+  template <class T>
+  T* ws(int slot, size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (ws_slots[slot].n < bytes) ws_slots[slot].alloc(bytes + bytes / 4, stream);
+    return reinterpret_cast<T*>(ws_slots[slot].p);
+  }
 };
 
 // ------------------------------------------------------------------- store
@@ -160,6 +170,8 @@ __global__ void k_block_norms(const double* vals, const int32_t* row_ptr, const 
                               int64_t nbr, double* out, int64_t nblk);
 void upload_sizes(Mat& m);
 void check_launch(const char* what);
+// implemented in bt_multiply.cu: C += A*B on one rank's stores (throws bt::Error)
+void local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& C, double eps, bt_stats* stats);
 
 }  // namespace bt
 

@@ -467,14 +467,9 @@ Plan plan_dmma(int cls, int ktmax) {
 
 using namespace bt;
 
-extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_mat* ch,
-                           double eps, bt_stats* stats) {
-  return guard([&] {
-    BT_REQUIRE(ctx && ah && bh && ch, BT_ERR_INVALID_ARGUMENT, "null argument");
-    Ctx& x = ctx->impl;
-    const Mat& A = ah->impl;
-    const Mat& B = bh->impl;
-    Mat& Cm = ch->impl;
+// The local multiply C += A*B (one rank's stores); throws bt::Error.
+void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps, bt_stats* stats) {
+  {
     BT_REQUIRE(A.ctx == &x && B.ctx == &x && Cm.ctx == &x, BT_ERR_INVALID_ARGUMENT,
                "bt_multiply: matrices belong to another context");
     // conformity (multiply_cannon.hpp:70-73, multiply_rect.hpp:106-112)
@@ -532,19 +527,22 @@ extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_m
     ra.dmma_ok = dmma_ok;
 
     // ---- pass 1: sizes (the one host synchronisation)
-    DBuf<int32_t> row_nnz(M + 1, st), out_rp(M + 1, st);
-    DBuf<int64_t> row_prod(M + 1, st), row_vals(M + 1, st), prod_base(M + 1, st),
-        val_base(M + 1, st);
-    DBuf<unsigned long long> tot(3 + NCLASS, st);
-    BT_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(unsigned long long) * (3 + NCLASS), st));
-    BT_CUDA(cudaMemsetAsync(row_nnz.p + M, 0, sizeof(int32_t), st));
-    BT_CUDA(cudaMemsetAsync(row_prod.p + M, 0, sizeof(int64_t), st));
-    BT_CUDA(cudaMemsetAsync(row_vals.p + M, 0, sizeof(int64_t), st));
-    ra.row_nnz = row_nnz.p;
-    ra.row_prod = row_prod.p;
-    ra.row_vals = row_vals.p;
-    ra.totals = tot.p;
-    ra.class_items = tot.p + 3;
+    DBuf<int32_t> out_rp(M + 1, st);
+    int32_t* row_nnz = x.ws<int32_t>(0, M + 1);
+    int64_t* row_prod = x.ws<int64_t>(1, M + 1);
+    int64_t* row_vals = x.ws<int64_t>(2, M + 1);
+    int64_t* prod_base = x.ws<int64_t>(3, M + 1);
+    int64_t* val_base = x.ws<int64_t>(4, M + 1);
+    unsigned long long* tot = x.ws<unsigned long long>(5, 3 + NCLASS);
+    BT_CUDA(cudaMemsetAsync(tot, 0, sizeof(unsigned long long) * (3 + NCLASS), st));
+    BT_CUDA(cudaMemsetAsync(row_nnz + M, 0, sizeof(int32_t), st));
+    BT_CUDA(cudaMemsetAsync(row_prod + M, 0, sizeof(int64_t), st));
+    BT_CUDA(cudaMemsetAsync(row_vals + M, 0, sizeof(int64_t), st));
+    ra.row_nnz = row_nnz;
+    ra.row_prod = row_prod;
+    ra.row_vals = row_vals;
+    ra.totals = tot;
+    ra.class_items = tot + 3;
     if (M > 0) {
       const size_t sm1 = static_cast<size_t>(N) * 4;
       if (sm1 > 48 * 1024)
@@ -555,25 +553,27 @@ extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_m
       count_launch(&x);
     }
     if (M <= 8192) {
-      k_scan_rows<<<1, 1024, 0, st>>>(row_nnz.p, row_prod.p, row_vals.p, M, out_rp.p, prod_base.p,
-                                      val_base.p);
+      k_scan_rows<<<1, 1024, 0, st>>>(row_nnz, row_prod, row_vals, M, out_rp.p, prod_base,
+                                      val_base);
       check_launch("scan_rows");
       count_launch(&x);
     } else {
-      exclusive_scan(x, row_nnz.p, out_rp.p, M + 1);
-      exclusive_scan(x, row_prod.p, prod_base.p, M + 1);
-      exclusive_scan(x, row_vals.p, val_base.p, M + 1);
+      exclusive_scan(x, row_nnz, out_rp.p, M + 1);
+      exclusive_scan(x, row_prod, prod_base, M + 1);
+      exclusive_scan(x, row_vals, val_base, M + 1);
     }
-    struct {
+    struct Sizes {
       int32_t nout;
       int32_t pad;
       int64_t nprod, nvals;
       unsigned long long tot[3 + NCLASS];
-    } h{};
+    };
+    static_assert(sizeof(Sizes) <= 4096, "pinned staging");
+    Sizes& h = *reinterpret_cast<Sizes*>(x.pinned);  // pinned: fast readback
     BT_CUDA(cudaMemcpyAsync(&h.nout, out_rp.p + M, 4, cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(&h.nprod, prod_base.p + M, 8, cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(&h.nvals, val_base.p + M, 8, cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(h.tot, tot.p, sizeof(h.tot), cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaMemcpyAsync(&h.nprod, prod_base + M, 8, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaMemcpyAsync(&h.nvals, val_base + M, 8, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaMemcpyAsync(h.tot, tot, sizeof(h.tot), cudaMemcpyDeviceToHost, st));
     BT_CUDA(cudaStreamSynchronize(st));
     const int64_t nout = h.nout, nprod = h.nprod, nvals = h.nvals;
     S.candidates = static_cast<int64_t>(h.tot[0]);
@@ -585,21 +585,23 @@ extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_m
                BT_ERR_INVALID_ARGUMENT, "multiply: operand slab exceeds 2^31 tiles");
 
     // ---- pass 2: C_out pattern, product stacks (descriptors)
-    DBuf<int32_t> out_col(std::max<int64_t>(nout, 1), st), out_row(std::max<int64_t>(nout, 1), st),
-        out_np(std::max<int64_t>(nout, 1), st);
-    DBuf<int64_t> out_off(std::max<int64_t>(nout, 1), st), cin_map(std::max<int64_t>(nout, 1), st),
-        out_p0(std::max<int64_t>(nout, 1), st);
-    DBuf<Desc> desc(std::max<int64_t>(nprod, 1), st);
+    DBuf<int32_t> out_col(std::max<int64_t>(nout, 1), st);
+    DBuf<int64_t> out_off(std::max<int64_t>(nout, 1), st);
+    int32_t* out_row = x.ws<int32_t>(6, nout);
+    int32_t* out_np = x.ws<int32_t>(7, nout);
+    int64_t* cin_map = x.ws<int64_t>(8, nout);
+    int64_t* out_p0 = x.ws<int64_t>(9, nout);
+    Desc* desc = x.ws<Desc>(10, nprod);
     ra.out_rp = out_rp.p;
-    ra.prod_base = prod_base.p;
-    ra.val_base = val_base.p;
+    ra.prod_base = prod_base;
+    ra.val_base = val_base;
     ra.out_col = out_col.p;
-    ra.out_row = out_row.p;
+    ra.out_row = out_row;
     ra.out_off = out_off.p;
-    ra.cin_map = cin_map.p;
-    ra.out_np = out_np.p;
-    ra.out_p0 = out_p0.p;
-    ra.desc = desc.p;
+    ra.cin_map = cin_map;
+    ra.out_np = out_np;
+    ra.out_p0 = out_p0;
+    ra.desc = desc;
     if (nout > 0) {
       if (row_smem > 48 * 1024)
         BT_CUDA(cudaFuncSetAttribute(k_row_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -638,55 +640,52 @@ extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_m
       const int sort_begin = band == 1 ? kb.cls : 0;
       BT_REQUIRE(kb.end <= 64, BT_ERR_INVALID_ARGUMENT, "multiply: item key overflow");
       const int32_t* ord = nullptr;  // identity: natural C entry order
-      DBuf<uint64_t> keys, keys_s;
-      DBuf<int32_t> order, order_s;
       if (kb.end > sort_begin) {
-        keys.alloc(nout, st);
-        keys_s.alloc(nout, st);
-        order.alloc(nout, st);
-        order_s.alloc(nout, st);
-        k_item_keys<<<blocks_for(nout, 256), 256, 0, st>>>(out_row.p, out_col.p, Cm.rsz.p,
-                                                           Cm.csz.p, nout, dmma_ok, band, kb,
-                                                           keys.p, order.p);
+        uint64_t* keys = x.ws<uint64_t>(11, nout);
+        uint64_t* keys_s = x.ws<uint64_t>(12, nout);
+        int32_t* order = x.ws<int32_t>(13, nout);
+        int32_t* order_s = x.ws<int32_t>(14, nout);
+        k_item_keys<<<blocks_for(nout, 256), 256, 0, st>>>(out_row, out_col.p, Cm.rsz.p, Cm.csz.p,
+                                                           nout, dmma_ok, band, kb, keys, order);
         check_launch("item_keys");
         count_launch(&x);
         size_t bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, keys_s.p, order.p, order_s.p,
-                                        nout, sort_begin, kb.end, st);
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys_s, order, order_s, nout,
+                                        sort_begin, kb.end, st);
         void* tmp = x.ensure_scratch(bytes);
-        cub::DeviceRadixSort::SortPairs(tmp, bytes, keys.p, keys_s.p, order.p, order_s.p, nout,
+        cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys_s, order, order_s, nout,
                                         sort_begin, kb.end, st);
         count_launch(&x, 2 + (kb.end - sort_begin + 7) / 8);
-        ord = order_s.p;
+        ord = order_s;
       }
-      DBuf<int32_t> ntiles(nout + 1, st);
-      DBuf<int64_t> tstart(nout + 1, st);
+      int32_t* ntiles = x.ws<int32_t>(15, nout + 1);
+      int64_t* tstart = x.ws<int64_t>(16, nout + 1);
       const bool tall = nitems != nout;  // some C blocks split into 32-row tiles
       if (tall) {
-        k_ntiles<<<blocks_for(nout + 1, 256), 256, 0, st>>>(ord, out_row.p, out_col.p, Cm.rsz.p,
-                                                            Cm.csz.p, nout, dmma_ok, ntiles.p);
+        k_ntiles<<<blocks_for(nout + 1, 256), 256, 0, st>>>(ord, out_row, out_col.p, Cm.rsz.p,
+                                                            Cm.csz.p, nout, dmma_ok, ntiles);
         count_launch(&x);
-        exclusive_scan(x, ntiles.p, tstart.p, nout + 1);
+        exclusive_scan(x, ntiles, tstart, nout + 1);
       }
-      DBuf<Item> items(std::max<int64_t>(nitems, 1), st);
-      k_build_items<<<blocks_for(nout, 256), 256, 0, st>>>(ord, tall ? ntiles.p : nullptr,
-                                                           tall ? tstart.p : nullptr, nout, out_row.p,
+      Item* items = x.ws<Item>(17, nitems);
+      k_build_items<<<blocks_for(nout, 256), 256, 0, st>>>(ord, tall ? ntiles : nullptr,
+                                                           tall ? tstart : nullptr, nout, out_row,
                                                            out_col.p, Cm.rsz.p, Cm.csz.p,
-                                                           out_off.p, cin_map.p, out_np.p,
-                                                           out_p0.p, items.p);
+                                                           out_off.p, cin_map, out_np, out_p0,
+                                                           items);
       check_launch("build_items");
       count_launch(&x);
 
       // ---- numeric phase
       NumArgs g{};
-      g.items = items.p;
-      g.desc = desc.p;
+      g.items = items;
+      g.desc = desc;
       g.at = A.vals.p;
       g.bt = B.vals.p;
       g.cin = Cm.vals.p;
       g.cout = new_vals.p;
-      DBuf<unsigned long long> counters(NCLASS, st);
-      BT_CUDA(cudaMemsetAsync(counters.p, 0, sizeof(unsigned long long) * NCLASS, st));
+      unsigned long long* counters = x.ws<unsigned long long>(18, NCLASS);
+      BT_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * NCLASS, st));
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[1], st));
       const int ktmax = std::max(1, tiles8(kmax));
       for (int q = 0; q < NCLASS; ++q) {
@@ -694,7 +693,7 @@ extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_m
         if (hi <= lo) continue;
         g.item_lo = lo;
         g.nitems = hi - lo;
-        g.counter = counters.p + q;
+        g.counter = counters + q;
         if (q == GENERIC) {
           k_smm_generic<<<static_cast<unsigned>(hi - lo), 128, 0, st>>>(g);
           check_launch("smm_generic");
@@ -739,5 +738,13 @@ extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_m
     S.c_blocks_out = nout;
     S.kernels = static_cast<int32_t>(x.kernels - k0);
     if (stats) *stats = S;
+  }
+}
+
+extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_mat* ch,
+                           double eps, bt_stats* stats) {
+  return guard([&] {
+    BT_REQUIRE(ctx && ah && bh && ch, BT_ERR_INVALID_ARGUMENT, "null argument");
+    local_multiply(ctx->impl, ah->impl, bh->impl, ch->impl, eps, stats);
   });
 }

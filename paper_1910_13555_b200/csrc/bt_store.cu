@@ -265,6 +265,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     cudaSetDevice(x.device);
     cudaStreamSynchronize(x.stream);
     x.scratch.release();
+    for (auto& w : x.ws_slots) w.release();
     cudaStreamSynchronize(x.stream);
     if (x.nccl) ncclCommDestroy(static_cast<ncclComm_t>(x.nccl));
     if (x.pinned) cudaFreeHost(x.pinned);

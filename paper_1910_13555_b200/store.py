@@ -85,10 +85,20 @@ class LocalStore:
         check(self.lib.bt_mat_create(ctx.h, len(self.rsz), ptr(self.rsz, _i32p), len(self.csz),
                                      ptr(self.csz, _i32p), C.byref(h)), "new_matrix")
         self.h = h
+        self.owned = True
         ctx._stores.add(self)
 
+    @classmethod
+    def borrow(cls, ctx: Context, handle, row_sizes, col_sizes) -> "LocalStore":
+        """Non-owning view of a store owned by a distributed matrix."""
+        s = cls.__new__(cls)
+        s.ctx, s.lib, s.h, s.owned = ctx, ctx.lib, handle, False
+        s.rsz = np.ascontiguousarray(row_sizes, dtype=np.int32)
+        s.csz = np.ascontiguousarray(col_sizes, dtype=np.int32)
+        return s
+
     def close(self):
-        if getattr(self, "h", None) and self.ctx.h:
+        if getattr(self, "h", None) and getattr(self, "owned", False) and self.ctx.h:
             self.lib.bt_mat_destroy(self.h)
         self.h = None
 
