@@ -200,12 +200,11 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1910_13555_b200.store import Context, LocalStore, multiply_local, unique_id
-    if world > 1:
-        from paper_1910_13555_b200 import dist as ring
+    from paper_1910_13555_b200 import dist as dd
 
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")
         obj = [unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx = Context(local, world, rank, obj[0])
@@ -215,32 +214,50 @@ def main():
     stream = torch.cuda.ExternalStream(ctx.stream)
     sz = np.full(NB, BS, np.int32)
 
-    # ---- inputs (host, pinned) -- A/C row slab of this rank, B K-slab of this rank
+    # ---- inputs (host, pinned): A/C row slab of this rank, B K-slab of this rank
     abi, abj, av = make_blocks(SEED_A, NB, NB, BS, OCC, row0=NB * rank)
-    chunk = -(-NB // world)   # ChunkPartition (partition.hpp:17-41)
-    kslab = [(min(NB, chunk * p), min(NB, chunk * (p + 1))) for p in range(world)]
-    k0, k1 = kslab[rank]
+    chunk = -(-NB // world)   # ChunkPartition (partition.hpp:17-41) of B's block rows
+    k0, k1 = min(NB, chunk * rank), min(NB, chunk * (rank + 1))
     bbi_all, bbj_all, bv_all = make_blocks(SEED_B, NB, NB, BS, OCC)
     sel = (bbi_all >= k0) & (bbi_all < k1)
     bsize = BS * BS
-    bidx = np.nonzero(sel)[0]
     bbi, bbj = bbi_all[sel], bbj_all[sel]
-    bv = bv_all.reshape(-1, bsize)[bidx].ravel()
+    bv = np.ascontiguousarray(bv_all.reshape(-1, bsize)[np.nonzero(sel)[0]].ravel())
     av_pin = torch.from_numpy(av).pin_memory()
-    bv_pin = torch.from_numpy(np.ascontiguousarray(bv)).pin_memory()
-
-    a = LocalStore(ctx, sz, sz)
-    a.put_blocks(abi, abj, av_pin)
-    b = LocalStore(ctx, sz, sz)
-    b.put_blocks(bbi, bbj, bv_pin)
-    c = LocalStore(ctx, sz, sz)
+    bv_pin = torch.from_numpy(bv).pin_memory()
     flops_rank = useful_flops_host(abi, abj, bbi_all, bbj_all, BS)
 
-    def step(cc):
-        cc.clear()
-        if world == 1:
+    if world == 1:
+        a = LocalStore(ctx, sz, sz)
+        a.put_blocks(abi, abj, av_pin)
+        b = LocalStore(ctx, sz, sz)
+        b.put_blocks(bbi, bbj, bv_pin)
+        c = LocalStore(ctx, sz, sz)
+
+        def step(cc):
+            cc.clear()
             return multiply_local(ctx, a, b, cc)
-        return ring.multiply_gather_b(ctx, a, b, cc)
+    else:
+        # weak scaling: A and C are 400*world x 400 block matrices in row slabs
+        # (rank r owns block rows [400 r, 400 r + 400)), B is 400 x 400 in K slabs;
+        # the layouts already match case 2's, so a step is the B gather over
+        # NVLink + the local multiply (multiply_rect.hpp:199-238)
+        comm = dd.SimComm.nccl(ctx)
+        grid = dd.ProcessGrid([world, 1])
+        rows_a = dd.Blocking.uniform(NB * world, BS)
+        cols = dd.Blocking.uniform(NB, BS)
+        a = dd.new_matrix(rows_a, cols, grid, np.arange(NB * world) // NB,
+                          np.zeros(NB, np.int64), comm)
+        a.put_blocks(abi + NB * rank, abj, av)
+        b = dd.new_matrix(cols, cols, grid, np.arange(NB) // chunk, np.zeros(NB, np.int64), comm)
+        b.put_blocks(bbi, bbj, bv)
+        c = dd.new_matrix(rows_a, cols, grid, np.arange(NB * world) // NB,
+                          np.zeros(NB, np.int64), comm)
+
+        def step(cc):
+            cc.local(rank).clear()
+            st = dd.multiply_virtual_case2(comm, a, b, cc, world, gather=True)
+            return st
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
@@ -274,7 +291,7 @@ def main():
     ms_local = float(np.mean(step_ms))
     ms = ms_local
     if world > 1:
-        t = torch.tensor([ms_local], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms_local], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     flops_step = stats[-1]["flops"]
@@ -295,26 +312,35 @@ def main():
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        ea = LocalStore(ctx, sz, sz)
-        ea.put_blocks(abi, abj, av_pin)
-        eb = LocalStore(ctx, sz, sz)
-        eb.put_blocks(bbi, bbj, bv_pin)
-        ec = LocalStore(ctx, sz, sz)
         if world == 1:
+            ea = LocalStore(ctx, sz, sz)
+            ea.put_blocks(abi, abj, av_pin)
+            eb = LocalStore(ctx, sz, sz)
+            eb.put_blocks(bbi, bbj, bv_pin)
+            ec = LocalStore(ctx, sz, sz)
             multiply_local(ctx, ea, eb, ec)
+            ci, cj, _ = ec.export(cout)
+            ctx.sync()
+            dt = time.perf_counter() - t0
+            d2h = 8 * int(ec.info()[1]) + 16 * len(ci)
+            for x in (ea, eb, ec):
+                x.close()
         else:
-            ring.multiply_gather_b(ctx, ea, eb, ec)
-        ci, cj, _ = ec.export(cout)
-        ctx.sync()
-        dt = time.perf_counter() - t0
-        d2h = 8 * int(ec.info()[1]) + 16 * len(ci)
-        for x in (ea, eb, ec):
-            x.close()
+            a.local(rank).clear()
+            b.local(rank).clear()
+            c.local(rank).clear()
+            a.local(rank).put_blocks(abi + NB * rank, abj, av_pin)
+            b.local(rank).put_blocks(bbi, bbj, bv_pin)
+            dd.multiply_virtual_case2(comm, a, b, c, world, gather=True)
+            ci, cj, _ = c.local(rank).export(cout)
+            ctx.sync()
+            dt = time.perf_counter() - t0
+            d2h = 8 * int(c.local(rank).info()[1]) + 16 * len(ci)
         if s >= args.warmup:
             e2e_times.append(dt)
     e2e_s = float(np.mean(e2e_times))
     if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_val = flops_step * world / e2e_s / 1e9
@@ -332,7 +358,8 @@ def main():
                 "products_per_rank": int(stats[-1]["products"]),
                 "useful_gflop_per_rank": round(flops_step / 1e9, 4),
                 "distribution": "single GPU" if world == 1 else
-                f"A/C row slabs per rank, B K-slab ring over NCCL ({world} ranks)",
+                f"case 2 weak scaling: A/C 400-block-row slabs per rank, B K-slabs "
+                f"gathered over NVLink/NCCL each step ({world} ranks)",
                 "l2": "flushed (256 MB write) before every timed step",
             },
             "roofline": {
@@ -353,8 +380,11 @@ def main():
             cb, _ = cpu_baseline_sample()
             line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)
-    for x in (a, b, c):
-        x.close()
+    if world > 1:
+        comm.close()
+    else:
+        for x in (a, b, c):
+            x.close()
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

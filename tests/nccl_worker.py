@@ -1,0 +1,116 @@
+"""Multi-process (one GPU per rank, NCCL over NVLink) parity worker.
+
+Run by tests/test_nccl_gpu.py as
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/nccl_worker.py
+Every rank builds the same seeded inputs, puts only the blocks it owns, runs
+the distributed drivers through the C-ABI (NCCL transport), gathers its C
+blocks to rank 0 over gloo, and rank 0 checks them against the oracle
+(pattern bit-exact, values <= 1e-12 Frobenius).  Exits non-zero on mismatch.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+from helpers import assert_parity  # noqa: E402
+from oracle.oracle import Blocks, Oracle  # noqa: E402
+from paper_1910_13555_b200 import dist as d  # noqa: E402
+from paper_1910_13555_b200.store import Context, unique_id  # noqa: E402
+
+
+def owned(blocks: Blocks, m):
+    """the blocks of `blocks` this process owns under m's layout"""
+    keep = [t for t in range(blocks.nblk) if m.owner_rank(int(blocks.bi[t]), int(blocks.bj[t]))
+            in m.comm.local_ranks()]
+    off = blocks.offsets()
+    vals = np.concatenate([blocks.vals[off[t]:off[t + 1]] for t in keep]) if keep else np.zeros(0)
+    return blocks.bi[keep], blocks.bj[keep], vals
+
+
+def build(blocks, grid, comm):
+    m = d.new_matrix_round_robin(d.Blocking(blocks.rsz), d.Blocking(blocks.csz), grid, comm)
+    bi, bj, v = owned(blocks, m)
+    if len(bi):
+        m.put_blocks(bi, bj, v)
+    return m
+
+
+def gather_c(c):
+    bi, bj, v = c.blocks()
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, (bi, bj, v))
+    if dist.get_rank() != 0:
+        return None
+    bi = np.concatenate([p[0] for p in parts])
+    bj = np.concatenate([p[1] for p in parts])
+    rs, cs = c.rows().sizes(), c.cols().sizes()
+    sizes = [rs[i] * cs[j] for p in parts for i, j in zip(p[0], p[1])]
+    vals_list = []
+    for p in parts:
+        off = 0
+        for i, j in zip(p[0], p[1]):
+            n = rs[i] * cs[j]
+            vals_list.append(p[2][off:off + n])
+            off += n
+    order = np.lexsort((bj, bi))
+    vals = np.concatenate([vals_list[t] for t in order]) if len(order) else np.zeros(0)
+    del sizes
+    return Blocks(rs, cs, bi[order], bj[order], vals)
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    obj = [unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx = Context(local, world, rank, obj[0])
+    comm = d.SimComm.nccl(ctx)
+    o = Oracle()
+    failures = 0
+    q = int(round(world ** 0.5))
+    cases = []
+    if q * q == world:
+        cases.append(("cannon", q))
+    cases += [("case1", 1), ("case2", 1), ("case2g", 1)]
+    rs = np.array([5, 13, 23, 7, 13, 5, 23, 11, 9, 17, 4, 23], np.int32)
+    ks = np.array([13, 5, 23, 8, 16, 23, 5, 13], np.int32)
+    ns = np.array([23, 7, 5, 13, 20, 9, 23], np.int32)
+    for algo, gq in cases:
+        A = o.random_matrix(11, rs, ks, 0.45)
+        B = o.random_matrix(12, ks, ns, 0.45)
+        Cin = o.random_matrix(13, rs, ns, 0.2)
+        grid = d.ProcessGrid([gq, gq])
+        a, b, c = build(A, grid, comm), build(B, grid, comm), build(Cin, grid, comm)
+        if algo == "cannon":
+            st = d.multiply_cannon(comm, a, b, c)
+        elif algo == "case1":
+            st = d.multiply_reduce_case1(comm, a, b, c, world)
+        else:
+            st = d.multiply_virtual_case2(comm, a, b, c, world, gather=(algo == "case2g"))
+        got = gather_c(c)
+        if rank == 0:
+            want, _, _ = o.multiply(A, B, Cin)
+            try:
+                err = assert_parity(got, want)
+                print(f"[nccl world={world}] {algo}: OK rel_err={err:.2e} "
+                      f"sent={st['elements_sent']}", flush=True)
+            except AssertionError as e:
+                failures += 1
+                print(f"[nccl world={world}] {algo}: FAIL {e}", flush=True)
+    flag = torch.tensor([failures])
+    dist.broadcast(flag, 0)
+    comm.close()
+    ctx.close()
+    dist.destroy_process_group()
+    sys.exit(1 if int(flag.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,30 @@
+"""NCCL transport: one process per GPU (torchrun), the drivers vs the oracle.
+
+Needs >= 2 GPUs (gpurun --gpus 2/4); skipped on a single-GPU box, where the
+same drivers are covered with virtual ranks by test_dist_gpu.py."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_nccl_drivers(world):
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29500 + world), os.path.join(HERE, "nccl_worker.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    print(p.stdout[-4000:])
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert p.stdout.count(": OK") >= 3
