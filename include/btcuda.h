@@ -169,6 +169,18 @@ int bt_multiply_case1(const bt_dmat* a, const bt_dmat* b, bt_dmat* c, int nprocs
 int bt_multiply_case2(const bt_dmat* a, const bt_dmat* b, bt_dmat* c, int nprocs, int gather,
                       double eps, bt_stats* stats);
 
+/* ------------------------------------------------------------ tensors */
+/* Tensor <-> matrix index remap (the reference has no tensor
+ * code).  A rank-ndim (2..4) block-sparse tensor with nblocks[d] blocks of sizes
+ * dim_sizes[d][...] along dimension d is stored as a matrix under a
+ * matricization map: dims[0..nrow) form the row group, dims[nrow..ndim) the
+ * column group, mixed radix with later-listed dimensions fastest, for block
+ * indices and for the elements inside a block.  Moves `src` (stored under the
+ * src map) into `dst` (blockings induced by the dst map), on the device. */
+int bt_tensor_remap(bt_ctx* ctx, int ndim, const int64_t* nblocks,
+                    const int32_t* const* dim_sizes, int src_nrow, const int* src_dims,
+                    const bt_mat* src, int dst_nrow, const int* dst_dims, bt_mat* dst);
+
 #ifdef __cplusplus
 }
 #endif

@@ -111,6 +111,9 @@ SIGNATURES = {
                                     C.POINTER(BtStats)]),
     "bt_multiply_case2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                     C.c_double, C.POINTER(BtStats)]),
+    "bt_tensor_remap": (C.c_int, [C.c_void_p, C.c_int, _i64p, C.POINTER(_i32p), C.c_int,
+                                  C.POINTER(C.c_int), C.c_void_p, C.c_int, C.POINTER(C.c_int),
+                                  C.c_void_p]),
 }
 
 _lib = None
