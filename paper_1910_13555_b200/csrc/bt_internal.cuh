@@ -161,6 +161,17 @@ __host__ __device__ inline int64_t t8_pos(int r, int c, int ntc) {
          ((c & 7) ^ (((r >> 1) & 1) << 2));
 }
 
+// BT_TRACE=1: host-side phase timings on stderr (development aid)
+struct Trace {
+  const char* what;
+  bool on;
+  double t0, last;
+  static double now();
+  explicit Trace(const char* w);
+  void mark(const char* phase);
+  ~Trace();
+};
+
 // launch accounting
 inline void count_launch(Ctx* c, int n = 1) { c->kernels += n; }
 

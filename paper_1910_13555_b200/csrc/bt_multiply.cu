@@ -398,25 +398,38 @@ inline int bits_for(int64_t v) {  // bits to represent values in [0, v)
 constexpr int kWarps = 4;
 using KernelFn = void (*)(const NumArgs);
 
-KernelFn dmma_kernel(int cls) {
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+template <int S>
+KernelFn dmma_kernel_s(int cls) {
   static const KernelFn table[16] = {
-      k_smm_dmma<1, 1, kWarps>, k_smm_dmma<1, 2, kWarps>, k_smm_dmma<1, 3, kWarps>,
-      k_smm_dmma<1, 4, kWarps>, k_smm_dmma<2, 1, kWarps>, k_smm_dmma<2, 2, kWarps>,
-      k_smm_dmma<2, 3, kWarps>, k_smm_dmma<2, 4, kWarps>, k_smm_dmma<3, 1, kWarps>,
-      k_smm_dmma<3, 2, kWarps>, k_smm_dmma<3, 3, kWarps>, k_smm_dmma<3, 4, kWarps>,
-      k_smm_dmma<4, 1, kWarps>, k_smm_dmma<4, 2, kWarps>, k_smm_dmma<4, 3, kWarps>,
-      k_smm_dmma<4, 4, kWarps>};
+      k_smm_dmma<1, 1, kWarps, S>, k_smm_dmma<1, 2, kWarps, S>, k_smm_dmma<1, 3, kWarps, S>,
+      k_smm_dmma<1, 4, kWarps, S>, k_smm_dmma<2, 1, kWarps, S>, k_smm_dmma<2, 2, kWarps, S>,
+      k_smm_dmma<2, 3, kWarps, S>, k_smm_dmma<2, 4, kWarps, S>, k_smm_dmma<3, 1, kWarps, S>,
+      k_smm_dmma<3, 2, kWarps, S>, k_smm_dmma<3, 3, kWarps, S>, k_smm_dmma<3, 4, kWarps, S>,
+      k_smm_dmma<4, 1, kWarps, S>, k_smm_dmma<4, 2, kWarps, S>, k_smm_dmma<4, 3, kWarps, S>,
+      k_smm_dmma<4, 4, kWarps, S>};
   return table[cls];
 }
 
-// cudaFuncSetAttribute + occupancy query, cached per (class, smem bytes)
+KernelFn dmma_kernel(int cls, int stages) {
+  return stages >= 2 ? dmma_kernel_s<2>(cls) : dmma_kernel_s<1>(cls);
+}
+
+// cudaFuncSetAttribute + occupancy query, cached per (kernel, smem bytes)
 int dmma_occupancy(int cls, KernelFn fn, size_t smem) {
+  static KernelFn cached_fn[16] = {nullptr};
   static size_t cached_smem[16] = {0};
   static int cached_occ[16] = {0};
   static int cached_dev[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
   int dev = 0;
   BT_CUDA(cudaGetDevice(&dev));
-  if (cached_smem[cls] == smem && cached_dev[cls] == dev) return cached_occ[cls];
+  if (cached_fn[cls] == fn && cached_smem[cls] == smem && cached_dev[cls] == dev)
+    return cached_occ[cls];
+  cached_fn[cls] = fn;
   BT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(smem)));
   int per_sm = 0;
@@ -434,11 +447,6 @@ struct Plan {
   size_t smem = 0;
 };
 
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
-
 // Shared-memory plan for one DMMA class: per warp `stages` buffers holding one
 // A slab (TMT x KT tiles) and one B block (KT x TNT tiles).  Measured on c1
 // (profiles/): resident warps matter more than ring depth, so the default is
@@ -453,11 +461,11 @@ Plan plan_dmma(int cls, int ktmax) {
   const int want_warps = env_int("BT_WARPS_PER_SM", 24);
   int s = env_int("BT_STAGES", 0);
   if (s <= 0) {
-    s = 4;
-    while (s > 1 && static_cast<size_t>(want_warps) * (s * per_stage + 512) > budget) --s;
+    s = 2;
+    while (s > 1 && static_cast<size_t>(want_warps) * (s * per_stage + 1536) > budget) --s;
   }
-  P.stages = std::max(1, std::min(s, 8));
-  P.smem = kWarps * 512 + static_cast<size_t>(kWarps) * P.stages * per_stage;
+  P.stages = std::max(1, std::min(s, 2));
+  P.smem = kWarps * 1536 + static_cast<size_t>(kWarps) * P.stages * per_stage;
   return P;
 }
 
@@ -704,7 +712,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         g.stages = P.stages;
         g.stage_doubles = P.stage_doubles;
         g.a_region = P.a_region;
-        KernelFn fn = dmma_kernel(q);
+        KernelFn fn = dmma_kernel(q, P.stages);
         const int per_sm = dmma_occupancy(q, fn, P.smem);
         BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
         const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,

@@ -61,108 +61,163 @@ __device__ __forceinline__ int item_r8(const Item& it) {
 // FP64 DMMA tile kernel: warp <-> C tile of up to TM = 8*TMT rows and exactly
 // TN = 8*TNT padded columns.
 //
-// Warps take tickets for items of the band-ordered list from a global counter,
-// so the warps running at any moment sit on neighbouring C tiles (shared A band
-// in L2) and finish together.  Producer side (issue of bulk copies) runs
-// `stages` products ahead of the consumer; tickets are drawn three items ahead,
-// item structs loaded two ahead and product descriptors one ahead (one
-// coalesced load, distributed by shuffles), so no dependent global load sits on
-// the DMMA critical path.
-#ifndef BT_DMMA_MINBLOCKS
-#define BT_DMMA_MINBLOCKS 1
-#endif
-template <int TMT, int TNT, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, BT_DMMA_MINBLOCKS) k_smm_dmma(const NumArgs g) {
-  constexpr int QN = 8;  // per-warp queue of items between producer and consumer
+// Warps take tickets for items of the ordered item list from a global
+// counter (load balance; the warps in flight work on neighbouring C tiles).
+// Producer side (lane 0 issues the bulk copies) runs `S` products ahead of the
+// consumer.  All producer bookkeeping lives in shared memory and is prefetched
+// with cp.async so no global-load latency sits on the DMMA critical path and
+// the register budget stays small enough for 20 resident warps per SM:
+//   * item structs: slot n % QN holds the n-th item of this warp; the struct of
+//     item n+2 is requested when item n starts, its ticket one item earlier;
+//   * product descriptors: streamed in chunks of 32 through two slots, the
+//     following chunk requested when a chunk starts.
+// Resident CTAs targeted by the register allocator: 5 x 4 warps for tiles up to
+// 24x24 (<= 96 registers, 20 warps/SM fit the shared-memory ring), 3 for larger.
+template <int TMT, int TNT>
+constexpr int dmma_min_blocks() {
+  return TMT * TNT <= 9 ? 5 : 3;
+}
+template <int TMT, int TNT, int WARPS, int S>
+__global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_smm_dmma(const NumArgs g) {
+  constexpr int QN = 8;     // item slots per warp
+  constexpr int CTL = 1536; // control block bytes per warp
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int gq = lane >> 2, tq = lane & 3;
-  const int S = g.stages;
   // per-lane T8 positions of the DMMA fragments (bt_internal.cuh layout)
   const int sw_g = ((gq >> 1) & 1) << 2;
   const int la0 = gq * 8 + (tq ^ sw_g), la1 = gq * 8 + ((4 + tq) ^ sw_g);  // A (g, 4h+t)
   const int swt = ((tq >> 1) & 1) << 2;
   const int lb0 = tq * 8 + (gq ^ swt), lb1 = (4 + tq) * 8 + (gq ^ swt);    // B (4h+t, g)
   const int lc = gq * 8 + ((2 * tq) ^ sw_g);                               // C (g, 2t..2t+1)
-  // per-warp control block (512 B): 8 mbarriers | 8 stage kc | QN items
-  unsigned char* ctl = smem + wid * 512;
+  // control block: mbarriers | stage kc | item slots | 2 descriptor chunks
+  unsigned char* ctl = smem + wid * CTL;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ctl);
   int* stage_kc = reinterpret_cast<int*>(ctl + 64);
-  Item* q_items = reinterpret_cast<Item*>(ctl + 256);
-  double* stages = reinterpret_cast<double*>(smem + WARPS * 512) +
+  Item* q_items = reinterpret_cast<Item*>(ctl + 128);
+  Desc* dring = reinterpret_cast<Desc*>(ctl + 512);  // [2][32]
+  double* stages = reinterpret_cast<double*>(smem + WARPS * CTL) +
                    static_cast<int64_t>(wid) * S * g.stage_doubles;
+  const Item* items = g.items + g.item_lo;
 
+  // ---- prologue: tickets for items 0 and 1, their structs, ticket for item 2
+  unsigned long long tk = 0;  // lane 0: ticket of the item two ahead
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
+    for (int n = 0; n < 2; ++n) {
+      const unsigned long long id = atomicAdd(g.counter, 1ull);
+      if (static_cast<int64_t>(id) < g.nitems) {
+        cp_async16(&q_items[n], &items[id]);
+        cp_async16(reinterpret_cast<char*>(&q_items[n]) + 16,
+                   reinterpret_cast<const char*>(&items[id]) + 16);
+      } else {
+        q_items[n].np = -1;  // end of work
+      }
+    }
+    tk = atomicAdd(g.counter, 1ull);
   }
+  cp_async_commit();
+  cp_async_wait_all();
   __syncwarp();
 
-  const Item* items = g.items + g.item_lo;
-  // Item pipeline (dynamic work distribution, three deep so that no atomic or
-  // dependent load result is consumed in the step that issued it):
-  //   id3: ticket from the global counter (atomic in flight)
-  //   n2 : item struct loading (id known)
-  //   n1 : struct ready, its product descriptors loading (one per lane)
-  auto ticket = [&]() -> int64_t {
-    unsigned long long v = 0;
-    if (lane == 0) v = atomicAdd(g.counter, 1ull);
-    return static_cast<int64_t>(__shfl_sync(0xffffffffu, v, 0));
+  // descriptor chunk streaming
+  int cs = 0;                  // slot of the chunk being issued from
+  int64_t c_base = -1;         // global desc index of dring[cs][0]
+  int pf_n = -1;               // prefetched chunk in dring[cs ^ 1]: item seq and offset
+  int64_t pf_base = -1;
+  auto load_chunk = [&](int slot, int64_t base, int cnt) {
+    if (lane < cnt) cp_async16(&dring[slot * 32 + lane], &g.desc[base + lane]);
   };
-  int64_t idx_n1 = ticket();
-  int64_t idx_n2 = ticket();
-  int64_t id3 = ticket();
-  Item n1{}, n2{};
-  Desc n1_desc = make_int4(0, 0, 0, 0);
-  if (idx_n1 < g.nitems) n1 = items[idx_n1];
-  if (idx_n2 < g.nitems) n2 = items[idx_n2];
-  if (idx_n1 < g.nitems && lane < n1.np) n1_desc = g.desc[item_p0(n1) + lane];
 
   uint32_t issued = 0, consumed = 0;
-  int qh = 0, qt = 0;
-  // producer's current item
-  int64_t p_pos = 0, p_end = 0, d_base = 0;
+  int s_issue = 0, s_cons = 0;
+  uint32_t cons_phase = 0;
+  int qh = 0, qt = 0;  // consumer / producer item sequence numbers
+  int64_t p_pos = 0, p_end = 0;
   int p_r8 = 0, p_mt = 0;
-  Desc p_desc = make_int4(0, 0, 0, 0);
   bool p_more = true;
+
+  // next chunk after (item seq n, desc index pos) -- returns false if unknown yet
+  auto following = [&](int n, int64_t pos, int64_t end, int& fn, int64_t& fbase, int& fcnt) {
+    if (pos + 32 < end) {
+      fn = n;
+      fbase = pos + 32;
+      fcnt = static_cast<int>(end - fbase < 32 ? end - fbase : 32);
+      return true;
+    }
+    const Item& nx = q_items[(n + 1) % QN];
+    if (nx.np <= 0) return false;
+    fn = n + 1;
+    fbase = item_p0(nx);
+    fcnt = min(32, nx.np);
+    return true;
+  };
+  // make dring[cs] hold the chunk starting at `pos` of item seq n
+  auto enter_chunk = [&](int n, int64_t pos, int64_t end) {
+    if (pf_base == pos && pf_n == n) {
+      cs ^= 1;  // prefetched
+    } else {     // slow path: load now
+      load_chunk(cs ^ 1, pos, static_cast<int>(end - pos < 32 ? end - pos : 32));
+      cs ^= 1;
+      cp_async_commit();
+    }
+    c_base = pos;
+    int fn;
+    int64_t fb;
+    int fc;
+    cp_async_wait_all();
+    __syncwarp();
+    if (following(n, pos, end, fn, fb, fc)) {
+      load_chunk(cs ^ 1, fb, fc);
+      pf_n = fn;
+      pf_base = fb;
+    } else {
+      pf_n = -1;
+      pf_base = -1;
+    }
+    cp_async_commit();
+  };
 
   auto top_up = [&]() {
     while (issued - consumed < static_cast<uint32_t>(S)) {
       if (p_pos >= p_end) {
-        if (!p_more || qt - qh >= QN) return;
-        if (idx_n1 >= g.nitems) {
+        // ---- start the next item (seq qt) if its slot pipeline allows
+        if (!p_more || qt + 2 - qh >= QN) return;
+        cp_async_wait_all();
+        __syncwarp();
+        const Item& it = q_items[qt % QN];
+        if (it.np < 0) {
           p_more = false;
           return;
         }
-        // advance: current <- n1, n1 <- n2 (+ its descs), n2 <- next struct
-        if (lane == 0) q_items[qt % QN] = n1;
+        // request the struct of item qt+2 (ticket drawn one item ago) and the
+        // ticket of item qt+3
+        if (lane == 0) {
+          Item* dst = &q_items[(qt + 2) % QN];
+          if (static_cast<int64_t>(tk) < g.nitems) {
+            cp_async16(dst, &items[tk]);
+            cp_async16(reinterpret_cast<char*>(dst) + 16,
+                       reinterpret_cast<const char*>(&items[tk]) + 16);
+            tk = atomicAdd(g.counter, 1ull);
+          } else {
+            dst->np = -1;
+          }
+        }
+        cp_async_commit();
+        p_pos = item_p0(it);
+        p_end = p_pos + it.np;
+        p_r8 = item_r8(it);
+        p_mt = (it.rows + 7) >> 3;
         ++qt;
-        p_pos = item_p0(n1);
-        p_end = p_pos + n1.np;
-        d_base = p_pos;
-        p_r8 = item_r8(n1);
-        p_mt = (n1.rows + 7) >> 3;
-        p_desc = n1_desc;
-        idx_n1 = idx_n2;
-        n1 = n2;
-        n1_desc = make_int4(0, 0, 0, 0);
-        if (idx_n1 < g.nitems && lane < n1.np) n1_desc = g.desc[item_p0(n1) + lane];
-        idx_n2 = id3;
-        if (idx_n2 < g.nitems) n2 = items[idx_n2];
-        id3 = idx_n2 < g.nitems ? ticket() : g.nitems;
+        if (p_pos < p_end) enter_chunk(qt - 1, p_pos, p_end);
         continue;
       }
-      if (p_pos - d_base >= 32) {  // items with more than 32 products
-        d_base = p_pos;
-        p_desc = lane < p_end - p_pos ? g.desc[p_pos + lane] : make_int4(0, 0, 0, 0);
-      }
-      const int src = static_cast<int>(p_pos - d_base);
-      Desc d;
-      d.x = __shfl_sync(0xffffffffu, p_desc.x, src);
-      d.y = __shfl_sync(0xffffffffu, p_desc.y, src);
-      d.z = __shfl_sync(0xffffffffu, p_desc.z, src);
-      const int s = static_cast<int>(issued % static_cast<uint32_t>(S));
+      if (p_pos - c_base >= 32) enter_chunk(qt - 1, p_pos, p_end);
+      const int s = s_issue;
+      s_issue = (s_issue + 1 == S) ? 0 : s_issue + 1;
       if (lane == 0) {
+        const Desc d = dring[cs * 32 + static_cast<int>(p_pos - c_base)];
         const int KT = (d.z + 1) >> 1;  // 8-wide k tiles
         const uint32_t ba = static_cast<uint32_t>(p_mt * KT) * 512u;
         const uint32_t bb = static_cast<uint32_t>(KT * TNT) * 512u;
@@ -206,8 +261,12 @@ __global__ void __launch_bounds__(WARPS * 32, BT_DMMA_MINBLOCKS) k_smm_dmma(cons
         }
     }
     for (int t = 0; t < it.np; ++t) {
-      const int s = static_cast<int>(consumed % static_cast<uint32_t>(S));
-      mbar_wait(&bars[s], (consumed / static_cast<uint32_t>(S)) & 1u);
+      const int s = s_cons;
+      mbar_wait(&bars[s], cons_phase);
+      if (++s_cons == S) {
+        s_cons = 0;
+        cons_phase ^= 1u;
+      }
       const int kc = stage_kc[s];
       const int KT = (kc + 1) >> 1;
       const double* sA = stages + static_cast<int64_t>(s) * g.stage_doubles;

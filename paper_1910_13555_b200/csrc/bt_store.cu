@@ -6,7 +6,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
+#include <ctime>
 #include <numeric>
 
 #include "bt_internal.cuh"
@@ -14,6 +16,29 @@
 namespace bt {
 
 static thread_local std::string g_last_error;
+
+double Trace::now() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+}
+Trace::Trace(const char* w) : what(w) {
+  static const bool enabled = [] {
+    const char* v = getenv("BT_TRACE");
+    return v && *v == '1';
+  }();
+  on = enabled;
+  t0 = last = on ? now() : 0.0;
+}
+void Trace::mark(const char* phase) {
+  if (!on) return;
+  const double t = now();
+  fprintf(stderr, "[bt-trace] %s %-18s %8.3f ms\n", what, phase, t - last);
+  last = t;
+}
+Trace::~Trace() {
+  if (on) fprintf(stderr, "[bt-trace] %s %-18s %8.3f ms\n", what, "TOTAL", now() - t0);
+}
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 void check_launch(const char* what) {
@@ -402,6 +427,7 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
     BT_REQUIRE(n >= 0, BT_ERR_INVALID_ARGUMENT, "negative block count");
     if (n == 0) return;
     BT_REQUIRE(bi && bj && vals, BT_ERR_INVALID_ARGUMENT, "null input arrays");
+    Trace tr("put");
     cudaStream_t st = m.stream();
     BT_CUDA(cudaSetDevice(m.ctx->device));
     // validate + compact input offsets
@@ -425,7 +451,9 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
       std::stable_sort(perm.begin(), perm.end(), [&](int64_t x, int64_t y) {
         return bi[x] != bi[y] ? bi[x] < bi[y] : bj[x] < bj[y];
       });
+    tr.mark("validate");
     HostIndex old = download_index(m);
+    tr.mark("download_index");
     // merge old pattern with batch keys
     std::vector<int32_t> row_ptr(m.nbr + 1, 0), col;
     std::vector<int64_t> off, old_off, inp_ptr{0}, inp_src;
@@ -474,9 +502,12 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
     for (int64_t i = 0; i < m.nbr; ++i) row_ptr[i + 1] += row_ptr[i];
     BT_REQUIRE(col.size() < (size_t(1) << 31), BT_ERR_INVALID_ARGUMENT,
                "store exceeds 2^31 blocks");
+    tr.mark("plan");
     // device: stage inputs, build new slab
     DBuf<double> d_in(in_total, st);
+    tr.mark("alloc_in");
     BT_CUDA(cudaMemcpyAsync(d_in.p, vals, sizeof(double) * in_total, cudaMemcpyHostToDevice, st));
+    tr.mark("h2d_enqueue");
     const int64_t nout = static_cast<int64_t>(col.size());
     DBuf<double> new_vals(std::max<int64_t>(nv, 2), st);
     BT_CUDA(cudaMemsetAsync(new_vals.p, 0, sizeof(double) * std::max<int64_t>(nv, 2), st));
@@ -489,9 +520,11 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
         new_vals.p, d_off.p, d_dims.p, m.vals.p, d_old.p, d_in.p, d_iptr.p, d_isrc.p, nout);
     check_launch("apply_put");
     count_launch(m.ctx);
+    tr.mark("kernel_enqueue");
     m.vals = std::move(new_vals);
     install_pattern(m, row_ptr, col, off, nv, ne);
     BT_CUDA(cudaStreamSynchronize(st));  // host buffers are borrowed for the call only
+    tr.mark("sync");
   });
 }
 
