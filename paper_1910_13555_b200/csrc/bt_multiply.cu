@@ -553,9 +553,13 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.class_items = tot + 3;
     if (M > 0) {
       const size_t sm1 = static_cast<size_t>(N) * 4;
-      if (sm1 > 48 * 1024)
+      // static + dynamic shared memory may exceed the 48 KB default: always opt in
+      static size_t set1 = 0;
+      if (sm1 > set1) {
         BT_CUDA(cudaFuncSetAttribute(k_row_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(sm1)));
+        set1 = sm1;
+      }
       k_row_count<<<static_cast<unsigned>(M), kChunkA, sm1, st>>>(ra);
       check_launch("row_count");
       count_launch(&x);
@@ -611,9 +615,12 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.out_p0 = out_p0;
     ra.desc = desc;
     if (nout > 0) {
-      if (row_smem > 48 * 1024)
+      static size_t set2 = 0;
+      if (row_smem > set2) {
         BT_CUDA(cudaFuncSetAttribute(k_row_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(row_smem)));
+        set2 = row_smem;
+      }
       k_row_fill<<<static_cast<unsigned>(M), kChunkA, row_smem, st>>>(ra);
       check_launch("row_fill");
       count_launch(&x);
