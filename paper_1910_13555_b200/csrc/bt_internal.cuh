@@ -104,6 +104,10 @@ struct Ctx {
   DBuf<unsigned char> scratch;  // CUB temp storage, reused
   void* pinned = nullptr;       // small pinned host staging for scalar readbacks
   bool timing = false;          // record CUDA events around multiply kernels
+  static constexpr int kAux = 4;  // side streams: concurrent per-class numeric kernels
+  cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_join[kAux] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   void* ensure_scratch(size_t bytes);
   // Grow-only per-slot workspace for call-local temporaries (no allocator calls

@@ -69,6 +69,9 @@ struct RowArgs {
   int32_t* out_np;  // products per C entry
   int64_t* out_p0;  // first product per C entry
   Desc* desc;
+  // work items, written by the fill pass into per-class segments
+  unsigned long long* class_cursor;  // [NCLASS], initialised to the segment bases
+  Item* items;
 };
 
 // Row walk helpers.  A(i,:) x B(k,:) pairs are enumerated load-balanced: the A
@@ -120,13 +123,20 @@ __device__ __forceinline__ int find_entry(const RowChunk& rc, int n, int32_t t) 
   return lo;
 }
 
-// cnt[j]: products of C(i,j) (kept by the eps filter) | kCinFlag for C_in blocks.
-__device__ void row_products(const RowArgs& g, int64_t i, uint32_t* cnt, RowChunk& rc,
-                             unsigned long long* cand, unsigned long long* mnk) {
+// cnt[j]: products of C(i,j) (kept by the eps filter) | kCinFlag for C_in blocks;
+// bits[j/32]: column j touched.  The column passes then visit touched columns
+// only (word by word), so their cost is O(N/32 + touched) per row.
+__device__ void row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_t* bits,
+                             RowChunk& rc, unsigned long long* cand, unsigned long long* mnk) {
+  const int nw = static_cast<int>((g.ncols + 31) >> 5);
   for (int64_t j = threadIdx.x; j < g.ncols; j += blockDim.x) cnt[j] = 0u;
+  for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0u;
   __syncthreads();
-  for (int32_t e = g.c_rp[i] + threadIdx.x; e < g.c_rp[i + 1]; e += blockDim.x)
-    cnt[g.c_col[e]] = kCinFlag;
+  for (int32_t e = g.c_rp[i] + threadIdx.x; e < g.c_rp[i + 1]; e += blockDim.x) {
+    const int32_t j = g.c_col[e];
+    cnt[j] = kCinFlag;
+    atomicOr(&bits[j >> 5], 1u << (j & 31));
+  }
   const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
   for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
     const int n = min(kChunkA, a1 - c0);
@@ -137,35 +147,75 @@ __device__ void row_products(const RowArgs& g, int64_t i, uint32_t* cnt, RowChun
       if (cand) ++*cand;
       if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
       const int32_t j = g.b_col[f];
-      atomicAdd(&cnt[j], 1u);
+      if (atomicAdd(&cnt[j], 1u) == 0u) atomicOr(&bits[j >> 5], 1u << (j & 31));
       if (mnk) *mnk += static_cast<unsigned long long>(g.k_sz[rc.k[l]]) * g.n_sz[j];
     }
     __syncthreads();
   }
 }
 
+// Warp-aggregated shared-memory atomicAdd: lanes adding to the same counter
+// (same class) are combined, one atomic per group; returns each lane's slot.
+__device__ __forceinline__ unsigned long long agg_add(unsigned long long* ctr, int key,
+                                                      unsigned long long v) {
+  const unsigned active = __activemask();
+  const unsigned peers = __match_any_sync(active, key);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  const unsigned below = peers & ((1u << lane) - 1u);
+  // all members of a group add the same v here (v depends on the key only)
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(ctr, v * static_cast<unsigned long long>(__popc(peers)));
+  base = __shfl_sync(peers, base, leader);
+  return base + v * static_cast<unsigned long long>(__popc(below));
+}
+
+// Touched columns of the row in ascending order -> tcol[0..n); returns n.
+__device__ int compact_touched(const uint32_t* bits, int nw, int32_t* tcol) {
+  using BS = cub::BlockScan<int, kChunkA>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int total;
+  int run = 0;
+  for (int w0 = 0; w0 < nw; w0 += blockDim.x) {
+    const int w = w0 + threadIdx.x;
+    const uint32_t word = w < nw ? bits[w] : 0u;
+    int ex, tot;
+    BS(tmp).ExclusiveSum(__popc(word), ex, tot);
+    int q = run + ex;
+    for (uint32_t x = word; x; x &= x - 1) tcol[q++] = w * 32 + __ffs(x) - 1;
+    run += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) total = run;
+  __syncthreads();
+  return total;
+}
+
 // Pass 1: per C block-row i -- number of C_out blocks, products, T8 slab size,
 // stored elements, per-class work items, useful flops.
 __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
   extern __shared__ uint32_t cnt[];
+  uint32_t* bits = cnt + g.ncols;
+  int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.ncols + 31) >> 5));
   __shared__ unsigned long long cls_items[NCLASS];
   __shared__ RowChunk rc;
   const int64_t i = blockIdx.x;
   if (threadIdx.x < NCLASS) cls_items[threadIdx.x] = 0;
   unsigned long long cand = 0, mnk = 0;
-  row_products(g, i, cnt, rc, &cand, &mnk);
+  row_products(g, i, cnt, bits, rc, &cand, &mnk);
   const int m = g.m_sz[i];
   long long nnz = 0, prods = 0, vals = 0, elems = 0;
-  for (int64_t j = threadIdx.x; j < g.ncols; j += blockDim.x) {
+  const int ntouch = compact_touched(bits, static_cast<int>((g.ncols + 31) >> 5), tcol);
+  for (int q = threadIdx.x; q < ntouch; q += blockDim.x) {
+    const int j = tcol[q];
     const uint32_t v = cnt[j];
-    if (!v) continue;
     const int n = g.n_sz[j];
     ++nnz;
     prods += v & ~kCinFlag;
     vals += t8_size(m, n);
     elems += static_cast<long long>(m) * n;
     const int cls = shape_class(m, n, g.dmma_ok);
-    atomicAdd(&cls_items[cls], static_cast<unsigned long long>(class_tiles(m, cls)));
+    agg_add(&cls_items[cls], cls, static_cast<unsigned long long>(class_tiles(m, cls)));
   }
   using BR = cub::BlockReduce<long long, kChunkA>;
   __shared__ typename BR::TempStorage tmp;
@@ -202,32 +252,39 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                                        // counts -> C entry rank
   int32_t* cur = reinterpret_cast<int32_t*>(sm + g.ncols);  // product cursor
+  uint32_t* bits = sm + 2 * g.ncols;                         // touched columns
   __shared__ RowChunk rc;
   __shared__ int32_t s_j[kPairCap];  // column of staged pair (-1: filtered out)
   __shared__ int32_t s_bu[kPairCap]; // B tile offset of staged pair
+  __shared__ unsigned long long cls_n[NCLASS], cls_at[NCLASS];
   const int64_t i = blockIdx.x;
-  row_products(g, i, cnt, rc, nullptr, nullptr);
+  if (threadIdx.x < NCLASS) cls_n[threadIdx.x] = 0;
+  row_products(g, i, cnt, bits, rc, nullptr, nullptr);
   const int m = g.m_sz[i];
   const int32_t cbase = g.out_rp[i];
   const int64_t pbase = g.prod_base[i], vbase = g.val_base[i];
+  int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.ncols + 31) >> 5));
+  const int ntouch = compact_touched(bits, static_cast<int>((g.ncols + 31) >> 5), tcol);
   {
+    // touched columns in ascending order, 256 at a time: ranks, product bases
+    // and T8 offsets by block scans
     using BS = cub::BlockScan<long long, kChunkA>;
     __shared__ typename BS::TempStorage tmp;
-    long long run_rank = 0, run_prod = 0, run_val = 0;
-    for (int64_t j0 = 0; j0 < g.ncols; j0 += blockDim.x) {
-      const int64_t j = j0 + threadIdx.x;
-      const uint32_t v = j < g.ncols ? cnt[j] : 0u;
-      const int n = (j < g.ncols && v) ? g.n_sz[j] : 0;
-      const long long present = v ? 1 : 0, np = v & ~kCinFlag, tv = v ? t8_size(m, n) : 0;
-      long long r_ex, p_ex, v_ex, r_tot, p_tot, v_tot;
-      BS(tmp).ExclusiveSum(present, r_ex, r_tot);
-      __syncthreads();
+    long long run_prod = 0, run_val = 0;
+    for (int q0 = 0; q0 < ntouch; q0 += blockDim.x) {
+      const int q = q0 + threadIdx.x;
+      const bool ok = q < ntouch;
+      const int j = ok ? tcol[q] : 0;
+      const uint32_t cj = ok ? cnt[j] : 0u;
+      const int n = ok ? g.n_sz[j] : 0;
+      const long long np = cj & ~kCinFlag, tv = ok ? t8_size(m, n) : 0;
+      long long p_ex, v_ex, p_tot, v_tot;
       BS(tmp).ExclusiveSum(np, p_ex, p_tot);
       __syncthreads();
       BS(tmp).ExclusiveSum(tv, v_ex, v_tot);
       __syncthreads();
-      if (v) {
-        const int32_t c = cbase + static_cast<int32_t>(run_rank + r_ex);
+      if (ok) {
+        const int32_t c = cbase + q;
         g.out_col[c] = static_cast<int32_t>(j);
         g.out_row[c] = static_cast<int32_t>(i);
         g.out_off[c] = vbase + run_val + v_ex;
@@ -235,17 +292,45 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         g.out_np[c] = static_cast<int32_t>(np);
         g.out_p0[c] = pbase + run_prod + p_ex;
         cur[j] = static_cast<int32_t>(run_prod + p_ex);
-        cnt[j] = static_cast<uint32_t>(run_rank + r_ex);
+        cnt[j] = static_cast<uint32_t>(q);
+        const int cls = shape_class(m, n, g.dmma_ok);
+        agg_add(&cls_n[cls], cls, static_cast<unsigned long long>(class_tiles(m, cls)));
       }
-      run_rank += r_tot;
       run_prod += p_tot;
       run_val += v_tot;
     }
   }
   __syncthreads();
+  // reserve this row's work items in every class segment (one atomic per class)
+  if (threadIdx.x < NCLASS) {
+    const unsigned long long k = cls_n[threadIdx.x];
+    cls_at[threadIdx.x] = k ? atomicAdd(&g.class_cursor[threadIdx.x], k) : 0ull;
+  }
+  __syncthreads();
   // C_in blocks: slot of the matching C_out block
   for (int32_t e = g.c_rp[i] + threadIdx.x; e < g.c_rp[i + 1]; e += blockDim.x)
     g.cin_map[cbase + cnt[g.c_col[e]]] = g.c_off[e];
+  __syncthreads();
+  // work items of this row: tall blocks become 32-row tiles
+  for (int32_t c = cbase + threadIdx.x; c < g.out_rp[i + 1]; c += blockDim.x) {
+    const int n = g.n_sz[g.out_col[c]];
+    const int cls = shape_class(m, n, g.dmma_ok);
+    const int nt = class_tiles(m, cls);
+    const unsigned long long at = agg_add(&cls_at[cls], cls, static_cast<unsigned long long>(nt));
+    const int64_t cin = g.cin_map[c];
+    const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
+    for (int q = 0; q < nt; ++q) {
+      const int r0 = 32 * q;
+      Item it;
+      it.c_off = g.out_off[c] + (r0 >> 3) * tile_row;
+      it.cin_off = cin >= 0 ? cin + (r0 >> 3) * tile_row : -1;
+      it.p0r8 = g.out_p0[c] | (static_cast<int64_t>(r0 >> 3) << 48);
+      it.np = g.out_np[c];
+      it.rows = static_cast<int16_t>(nt > 1 ? min(32, m - r0) : m);
+      it.n = static_cast<int16_t>(n);
+      g.items[at + q] = it;
+    }
+  }
   // products, k ascending
   const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
   for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
@@ -315,66 +400,6 @@ __global__ void __launch_bounds__(1024) k_scan_rows(const int32_t* __restrict__ 
   }
 }
 
-// ---- work items in L2-friendly band order
-struct KeyBits {
-  int col, band, cls, end;  // bit offsets (row-in-band at bit 0)
-};
-
-__global__ void k_item_keys(const int32_t* __restrict__ c_row, const int32_t* __restrict__ c_col,
-                            const int32_t* __restrict__ m_sz, const int32_t* __restrict__ n_sz,
-                            int64_t n, bool dmma_ok, int band, KeyBits kb,
-                            uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  const int32_t i = c_row[c], j = c_col[c];
-  const uint64_t cls = static_cast<uint64_t>(shape_class(m_sz[i], n_sz[j], dmma_ok));
-  keys[c] = (cls << kb.cls) | (static_cast<uint64_t>(i / band) << kb.band) |
-            (static_cast<uint64_t>(j) << kb.col) | static_cast<uint64_t>(i % band);
-  vals[c] = static_cast<int32_t>(c);
-}
-
-__global__ void k_ntiles(const int32_t* __restrict__ order, const int32_t* __restrict__ c_row,
-                         const int32_t* __restrict__ c_col, const int32_t* __restrict__ m_sz,
-                         const int32_t* __restrict__ n_sz, int64_t n, bool dmma_ok,
-                         int32_t* __restrict__ ntiles) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t > n) return;
-  if (t == n) {
-    ntiles[t] = 0;
-    return;
-  }
-  const int32_t c = order ? order[t] : static_cast<int32_t>(t);
-  const int m = m_sz[c_row[c]];
-  ntiles[t] = class_tiles(m, shape_class(m, n_sz[c_col[c]], dmma_ok));
-}
-
-__global__ void k_build_items(const int32_t* __restrict__ order, const int32_t* __restrict__ ntiles,
-                              const int64_t* __restrict__ tstart, int64_t n,
-                              const int32_t* __restrict__ c_row, const int32_t* __restrict__ c_col,
-                              const int32_t* __restrict__ m_sz, const int32_t* __restrict__ n_sz,
-                              const int64_t* __restrict__ c_off, const int64_t* __restrict__ cin_map,
-                              const int32_t* __restrict__ np, const int64_t* __restrict__ p0,
-                              Item* __restrict__ items) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const int32_t c = order ? order[t] : static_cast<int32_t>(t);
-  const int m = m_sz[c_row[c]], nn = n_sz[c_col[c]];
-  const int nt = ntiles ? ntiles[t] : 1;
-  const int64_t cin = cin_map[c];
-  const int64_t tile_row = static_cast<int64_t>(tiles8(nn)) * 64;  // doubles per 8-row strip
-  for (int q = 0; q < nt; ++q) {
-    const int r0 = 32 * q;
-    Item it;
-    it.c_off = c_off[c] + (r0 >> 3) * tile_row;
-    it.cin_off = cin >= 0 ? cin + (r0 >> 3) * tile_row : -1;
-    it.p0r8 = p0[c] | (static_cast<int64_t>(r0 >> 3) << 48);
-    it.np = np[c];
-    it.rows = static_cast<int16_t>(nt > 1 ? min(32, m - r0) : m);
-    it.n = static_cast<int16_t>(nn);
-    items[(tstart ? tstart[t] : t) + q] = it;
-  }
-}
-
 // ------------------------------------------------------------------- host
 namespace {
 
@@ -389,11 +414,6 @@ void exclusive_scan(Ctx& x, const TIn* in, TOut* out, int64_t n) {
 
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
-inline int bits_for(int64_t v) {  // bits to represent values in [0, v)
-  int b = 0;
-  while ((int64_t(1) << b) < v) ++b;
-  return b;
-}
 
 constexpr int kWarps = 4;
 using KernelFn = void (*)(const NumArgs);
@@ -494,9 +514,10 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     S.c_blocks_in = Cm.nblk;
     if (x.timing) BT_CUDA(cudaEventRecord(x.ev[0], st));
     const int64_t M = Cm.nbr, N = Cm.nbc;
-    const size_t row_smem = static_cast<size_t>(N) * 8;  // fill pass: 2 ints per column
-    BT_REQUIRE(row_smem <= 160 * 1024, BT_ERR_INVALID_ARGUMENT,
-               "multiply: more than 20480 block columns per C row is not supported");
+    // fill pass: 3 ints per column (counts, cursors, touched list) + bitmap
+    const size_t row_smem = static_cast<size_t>(N) * 12 + 4 * ((N + 31) / 32);
+    BT_REQUIRE(row_smem <= 180 * 1024, BT_ERR_INVALID_ARGUMENT,
+               "multiply: more than 15000 block columns per C row is not supported");
 
     // ---- norms for the eps filter
     DBuf<double> na, nb;
@@ -552,7 +573,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.totals = tot;
     ra.class_items = tot + 3;
     if (M > 0) {
-      const size_t sm1 = static_cast<size_t>(N) * 4;
+      const size_t sm1 = static_cast<size_t>(N) * 8 + 4 * ((N + 31) / 32);
       // static + dynamic shared memory may exceed the 48 KB default: always opt in
       static size_t set1 = 0;
       if (sm1 > set1) {
@@ -614,6 +635,21 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.out_np = out_np;
     ra.out_p0 = out_p0;
     ra.desc = desc;
+    // work-item segments per tile class (sizes from pass 1)
+    std::array<int64_t, NCLASS + 1> ibound{};
+    for (int q = 0; q < NCLASS; ++q) ibound[q + 1] = ibound[q] + static_cast<int64_t>(h.tot[3 + q]);
+    const int64_t nitems = ibound[NCLASS];
+    Item* items = x.ws<Item>(17, nitems);
+    unsigned long long* cursor = x.ws<unsigned long long>(18, 2 * NCLASS);
+    {
+      unsigned long long* hc = reinterpret_cast<unsigned long long*>(x.pinned) + 256;
+      for (int q = 0; q < NCLASS; ++q) hc[q] = static_cast<unsigned long long>(ibound[q]);
+      for (int q = 0; q < NCLASS; ++q) hc[NCLASS + q] = 0ull;  // ticket counters
+      BT_CUDA(cudaMemcpyAsync(cursor, hc, sizeof(unsigned long long) * 2 * NCLASS,
+                              cudaMemcpyHostToDevice, st));
+    }
+    ra.class_cursor = cursor;
+    ra.items = items;
     if (nout > 0) {
       static size_t set2 = 0;
       if (row_smem > set2) {
@@ -626,72 +662,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       count_launch(&x);
     }
 
-    // ---- work items: class | band | column | row-in-band order
+    // ---- numeric phase: one kernel per tile class, classes run concurrently
     DBuf<double> new_vals(std::max<int64_t>(nvals, 64), st);
     if (nout > 0) {
-      std::array<int64_t, NCLASS + 1> ibound{};
-      int nclasses = 0;
-      for (int q = 0; q < NCLASS; ++q) {
-        ibound[q + 1] = ibound[q] + static_cast<int64_t>(h.tot[3 + q]);
-        nclasses += h.tot[3 + q] > 0;
-      }
-      const int64_t nitems = ibound[NCLASS];
-      // band of A rows whose T8 blocks fill ~24 MB of L2
-      const double row_bytes = A.nbr ? 8.0 * static_cast<double>(A.nvals) / A.nbr : 1.0;
-      int band = static_cast<int>(std::min<double>(static_cast<double>(std::max<int64_t>(M, 1)),
-                                                   std::max(1.0, 24e6 / std::max(row_bytes, 1.0))));
-      band = std::max(1, env_int("BT_BAND", 0));
-      // Measured on c1 (profiles/r01_notes.md): band ordering is neutral when A+B fit
-      // in L2, so the default is natural row-major order (band = 1) -- no sort at
-      // all for a single shape class; BT_BAND=<rows> re-enables banding.
-      if (band <= 1) band = 1;
-      (void)row_bytes;
-      KeyBits kb;
-      kb.col = bits_for(band);
-      kb.band = kb.col + bits_for(N);
-      kb.cls = kb.band + bits_for((M + band - 1) / band);
-      kb.end = kb.cls + (nclasses > 1 ? 5 : 0);
-      // band == 1 keys follow the natural C entry order: sort only by class
-      const int sort_begin = band == 1 ? kb.cls : 0;
-      BT_REQUIRE(kb.end <= 64, BT_ERR_INVALID_ARGUMENT, "multiply: item key overflow");
-      const int32_t* ord = nullptr;  // identity: natural C entry order
-      if (kb.end > sort_begin) {
-        uint64_t* keys = x.ws<uint64_t>(11, nout);
-        uint64_t* keys_s = x.ws<uint64_t>(12, nout);
-        int32_t* order = x.ws<int32_t>(13, nout);
-        int32_t* order_s = x.ws<int32_t>(14, nout);
-        k_item_keys<<<blocks_for(nout, 256), 256, 0, st>>>(out_row, out_col.p, Cm.rsz.p, Cm.csz.p,
-                                                           nout, dmma_ok, band, kb, keys, order);
-        check_launch("item_keys");
-        count_launch(&x);
-        size_t bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys_s, order, order_s, nout,
-                                        sort_begin, kb.end, st);
-        void* tmp = x.ensure_scratch(bytes);
-        cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys_s, order, order_s, nout,
-                                        sort_begin, kb.end, st);
-        count_launch(&x, 2 + (kb.end - sort_begin + 7) / 8);
-        ord = order_s;
-      }
-      int32_t* ntiles = x.ws<int32_t>(15, nout + 1);
-      int64_t* tstart = x.ws<int64_t>(16, nout + 1);
-      const bool tall = nitems != nout;  // some C blocks split into 32-row tiles
-      if (tall) {
-        k_ntiles<<<blocks_for(nout + 1, 256), 256, 0, st>>>(ord, out_row, out_col.p, Cm.rsz.p,
-                                                            Cm.csz.p, nout, dmma_ok, ntiles);
-        count_launch(&x);
-        exclusive_scan(x, ntiles, tstart, nout + 1);
-      }
-      Item* items = x.ws<Item>(17, nitems);
-      k_build_items<<<blocks_for(nout, 256), 256, 0, st>>>(ord, tall ? ntiles : nullptr,
-                                                           tall ? tstart : nullptr, nout, out_row,
-                                                           out_col.p, Cm.rsz.p, Cm.csz.p,
-                                                           out_off.p, cin_map, out_np, out_p0,
-                                                           items);
-      check_launch("build_items");
-      count_launch(&x);
-
-      // ---- numeric phase
       NumArgs g{};
       g.items = items;
       g.desc = desc;
@@ -699,18 +672,29 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       g.bt = B.vals.p;
       g.cin = Cm.vals.p;
       g.cout = new_vals.p;
-      unsigned long long* counters = x.ws<unsigned long long>(18, NCLASS);
-      BT_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * NCLASS, st));
+      unsigned long long* counters = cursor + NCLASS;
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[1], st));
       const int ktmax = std::max(1, tiles8(kmax));
+      int nclasses = 0;
+      for (int q = 0; q < NCLASS; ++q) nclasses += ibound[q + 1] > ibound[q];
+      // several classes (mixed block sizes): fork onto the side streams so the
+      // small per-class grids fill the GPU together
+      const bool fork = nclasses > 1;
+      if (fork) {
+        BT_CUDA(cudaEventRecord(x.ev_fork, st));
+        for (auto& a : x.aux) BT_CUDA(cudaStreamWaitEvent(a, x.ev_fork, 0));
+      }
+      int launched = 0;
       for (int q = 0; q < NCLASS; ++q) {
         const int64_t lo = ibound[q], hi = ibound[q + 1];
         if (hi <= lo) continue;
+        cudaStream_t ks = fork ? x.aux[launched % Ctx::kAux] : st;
+        ++launched;
         g.item_lo = lo;
         g.nitems = hi - lo;
         g.counter = counters + q;
         if (q == GENERIC) {
-          k_smm_generic<<<static_cast<unsigned>(hi - lo), 128, 0, st>>>(g);
+          k_smm_generic<<<static_cast<unsigned>(hi - lo), 128, 0, ks>>>(g);
           check_launch("smm_generic");
           count_launch(&x);
           continue;
@@ -724,10 +708,15 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
         const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,
                                                (hi - lo + kWarps - 1) / kWarps);
-        fn<<<static_cast<unsigned>(grid), kWarps * 32, P.smem, st>>>(g);
+        fn<<<static_cast<unsigned>(grid), kWarps * 32, P.smem, ks>>>(g);
         check_launch("smm_dmma");
         count_launch(&x);
       }
+      if (fork)
+        for (int a = 0; a < Ctx::kAux; ++a) {
+          BT_CUDA(cudaEventRecord(x.ev_join[a], x.aux[a]));
+          BT_CUDA(cudaStreamWaitEvent(st, x.ev_join[a], 0));
+        }
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[2], st));
     }
 

@@ -267,6 +267,9 @@ int bt_ctx_create(int device, int nranks, int rank, const void* nccl_id, bt_ctx*
     BT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     BT_CUDA(cudaMallocHost(&x.pinned, 4096));
     for (auto& e : x.ev) BT_CUDA(cudaEventCreate(&e));
+    for (auto& a : x.aux) BT_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+    BT_CUDA(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming));
+    for (auto& e : x.ev_join) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (nranks > 1) {
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, 128);
@@ -295,6 +298,11 @@ int bt_ctx_destroy(bt_ctx* c) {
     if (x.nccl) ncclCommDestroy(static_cast<ncclComm_t>(x.nccl));
     if (x.pinned) cudaFreeHost(x.pinned);
     for (auto& e : x.ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& a : x.aux)
+      if (a) cudaStreamDestroy(a);
+    if (x.ev_fork) cudaEventDestroy(x.ev_fork);
+    for (auto& e : x.ev_join)
       if (e) cudaEventDestroy(e);
     cudaStreamDestroy(x.stream);
     delete c;
