@@ -263,10 +263,14 @@ struct Grid {
   int first = 0, nlocal = 1;
   bool nccl = false;
   cudaStream_t comm = nullptr;
-  cudaEvent_t ev_comm = nullptr, ev_main = nullptr;
+  cudaEvent_t ev_comm = nullptr, ev_main = nullptr, ev_idx = nullptr;
   std::vector<Counters> totals;
   std::vector<std::map<std::string, Counters>> phases;
   std::vector<std::string> phase;
+  // persistent buffers of the overlapped B gather (grow-only, reused per call)
+  std::unique_ptr<bt_mat> gather_full;
+  std::vector<DBuf<int32_t>> gather_rps;
+  DBuf<int64_t> gather_sizes;
   bool is_local(int r) const { return r >= first && r < first + nlocal; }
   void set_phase(const std::string& p) {
     for (int r = first; r < first + nlocal; ++r) phase[r] = p;
@@ -595,9 +599,10 @@ void add_stats(bt_stats& acc, const bt_stats& s) {
   acc.ms_total += s.ms_total;
 }
 
-void rank_multiply(Ctx* ctx, const Mat& a, const Mat& b, Mat& c, double eps, bt_stats& acc) {
+void rank_multiply(Ctx* ctx, const Mat& a, const Mat& b, Mat& c, double eps, bt_stats& acc,
+                   cudaEvent_t wait_numeric = nullptr) {
   bt_stats s{};
-  local_multiply(*ctx, a, b, c, eps, &s);
+  local_multiply(*ctx, a, b, c, eps, &s, wait_numeric);
   add_stats(acc, s);
 }
 
@@ -701,6 +706,121 @@ void concat_rows(const std::vector<const Mat*>& parts, const std::vector<int32_t
   out.nblk = nblk;
   out.nvals = nvals;
   out.nelems = nel;
+}
+
+// All-gather of row slabs over NCCL into one store, values overlapped: the
+// index (row_ptr/col/off) is exchanged first and assembled synchronously; the
+// values of every slab are then received straight into their place in the
+// full slab on the comm stream.  Returns an event recorded when the values have
+// landed; the local multiply's symbolic passes run meanwhile.
+cudaEvent_t gather_rows_nccl(Grid& g, const Mat& mine, const std::vector<int32_t>& rdist, int nprocs,
+                             Mat& full) {
+  Ctx& x = *g.ctx;
+  Trace tr("gather");
+  ncclComm_t comm = static_cast<ncclComm_t>(x.nccl);
+  const int me = g.first;
+  cudaStream_t cs = g.comm;
+  // sizes of every slab (3 words each)
+  auto grow = [&](auto& buf, size_t n) {
+    if (buf.n < n) buf.alloc(n + n / 8, x.stream);
+  };
+  grow(g.gather_sizes, static_cast<size_t>(3 * nprocs));
+  DBuf<int64_t>& dsz = g.gather_sizes;
+  int64_t* h = reinterpret_cast<int64_t*>(x.pinned) + 64;
+  h[0] = mine.nblk;
+  h[1] = mine.nvals;
+  h[2] = mine.nelems;
+  BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
+  BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
+  BT_CUDA(cudaMemcpyAsync(dsz.p + 3 * me, h, 24, cudaMemcpyHostToDevice, cs));
+  ncclResult_t r = ncclAllGather(dsz.p + 3 * me, dsz.p, 3, ncclInt64, comm, cs);
+  BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL size gather: ") + ncclGetErrorString(r));
+  BT_CUDA(cudaMemcpyAsync(h + 8, dsz.p, 24 * nprocs, cudaMemcpyDeviceToHost, cs));
+  BT_CUDA(cudaStreamSynchronize(cs));
+  tr.mark("sizes");
+  std::vector<int64_t> bb(nprocs + 1, 0), vb(nprocs + 1, 0);
+  int64_t nel = 0;
+  for (int p = 0; p < nprocs; ++p) {
+    bb[p + 1] = bb[p] + h[8 + 3 * p];
+    vb[p + 1] = vb[p] + h[8 + 3 * p + 1];
+    nel += h[8 + 3 * p + 2];
+  }
+  grow(full.row_ptr, static_cast<size_t>(full.nbr + 1));
+  grow(full.col, static_cast<size_t>(std::max<int64_t>(bb[nprocs], 1)));
+  grow(full.off, static_cast<size_t>(std::max<int64_t>(bb[nprocs], 1)));
+  grow(full.vals, static_cast<size_t>(std::max<int64_t>(vb[nprocs], 64)));
+  full.nblk = bb[nprocs];
+  full.nvals = vb[nprocs];
+  full.nelems = nel;
+  if (static_cast<int>(g.gather_rps.size()) < nprocs) g.gather_rps.resize(nprocs);
+  std::vector<DBuf<int32_t>>& rps = g.gather_rps;
+  for (int p = 0; p < nprocs; ++p) grow(rps[p], static_cast<size_t>(full.nbr + 1));
+  tr.mark("alloc");
+  BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
+  BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
+  // index round
+  BT_CUDA(cudaMemcpyAsync(rps[me].p, mine.row_ptr.p, 4 * (full.nbr + 1), cudaMemcpyDeviceToDevice, cs));
+  if (mine.nblk) {
+    BT_CUDA(cudaMemcpyAsync(full.col.p + bb[me], mine.col.p, 4 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
+    BT_CUDA(cudaMemcpyAsync(full.off.p + bb[me], mine.off.p, 8 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
+  }
+  ncclGroupStart();
+  for (int p = 0; p < nprocs; ++p) {
+    if (p == me) continue;
+    ncclSend(mine.row_ptr.p, full.nbr + 1, ncclInt32, p, comm, cs);
+    if (mine.nblk) {
+      ncclSend(mine.col.p, mine.nblk, ncclInt32, p, comm, cs);
+      ncclSend(mine.off.p, mine.nblk, ncclInt64, p, comm, cs);
+    }
+    const int64_t n = bb[p + 1] - bb[p];
+    ncclRecv(rps[p].p, full.nbr + 1, ncclInt32, p, comm, cs);
+    if (n) {
+      ncclRecv(full.col.p + bb[p], n, ncclInt32, p, comm, cs);
+      ncclRecv(full.off.p + bb[p], n, ncclInt64, p, comm, cs);
+    }
+  }
+  r = ncclGroupEnd();
+  BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL index round: ") + ncclGetErrorString(r));
+  BT_CUDA(cudaEventRecord(g.ev_idx, cs));
+  // values round (left in flight)
+  if (mine.nvals)
+    BT_CUDA(cudaMemcpyAsync(full.vals.p + vb[me], mine.vals.p, 8 * mine.nvals,
+                            cudaMemcpyDeviceToDevice, cs));
+  ncclGroupStart();
+  for (int p = 0; p < nprocs; ++p) {
+    if (p == me) continue;
+    if (mine.nvals) ncclSend(mine.vals.p, mine.nvals, ncclFloat64, p, comm, cs);
+    const int64_t nv = vb[p + 1] - vb[p];
+    if (nv) ncclRecv(full.vals.p + vb[p], nv, ncclFloat64, p, comm, cs);
+  }
+  r = ncclGroupEnd();
+  BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL value round: ") + ncclGetErrorString(r));
+  BT_CUDA(cudaEventRecord(g.ev_comm, cs));
+  tr.mark("enqueue rounds");
+  // assemble the index on the main stream once the index round is in; the
+  // values keep streaming on the comm stream
+  BT_CUDA(cudaStreamWaitEvent(x.stream, g.ev_idx, 0));
+  for (int p = 0; p < nprocs; ++p) {
+    int64_t r0 = -1, r1 = -1;
+    for (int64_t i = 0; i < full.nbr; ++i)
+      if (rdist[i] == p) {
+        if (r0 < 0) r0 = i;
+        r1 = i + 1;
+      }
+    if (r0 < 0) continue;
+    BT_CUDA(cudaMemcpyAsync(full.row_ptr.p + r0, rps[p].p + r0, 4 * (r1 - r0 + 1),
+                            cudaMemcpyDeviceToDevice, x.stream));
+    if (bb[p]) k_shift_rows<<<nb(r1 - r0 + 1, 256), 256, 0, x.stream>>>(full.row_ptr.p, r0, r1,
+                                                                         static_cast<int32_t>(bb[p]));
+    const int64_t n = bb[p + 1] - bb[p];
+    if (vb[p] && n) k_shift_off<<<nb(n, 256), 256, 0, x.stream>>>(full.off.p + bb[p], n, vb[p]);
+    count_launch(&x, 2);
+  }
+  BT_CUDA(cudaMemsetAsync(full.row_ptr.p, 0, 4, x.stream));
+  tr.mark("assemble");
+  g.charge_send(me, (nprocs - 1) * mine.nelems, (nprocs - 1) * 4 * mine.nblk);
+  g.charge_recv(me, nel - mine.nelems, 4 * (bb[nprocs] - mine.nblk));
+  return g.ev_comm;
 }
 
 }  // namespace
@@ -836,7 +956,15 @@ void case2(const DMat& a, const DMat& b, DMat& c, int nprocs, int gather, double
     cl = cl_owned.get();
   }
   g.set_phase("ring");
-  if (gather) {
+  if (gather && g.nccl && g.first < nprocs) {
+    // NCCL: index first, values overlapped with the symbolic passes
+    const int r = g.first;
+    if (!g.gather_full || g.gather_full->impl.h_rsz != b.rsz || g.gather_full->impl.h_csz != b.csz)
+      g.gather_full = new_store(g.ctx, b.rsz, b.csz);
+    Mat& full = g.gather_full->impl;
+    cudaEvent_t vals_ready = gather_rows_nccl(g, bl.view->store(r), ks, nprocs, full);
+    rank_multiply(g.ctx, al.view->store(r), full, cl->store(r), eps, S, vals_ready);
+  } else if (gather) {
     // all-gather of the B slabs
     std::vector<std::vector<std::unique_ptr<bt_mat>>> got(g.nlocal);
     std::vector<Send> sends;
@@ -934,6 +1062,7 @@ int bt_grid_create(bt_ctx* ctx, int nranks, bt_grid** out) {
     }
     BT_CUDA(cudaEventCreateWithFlags(&G.ev_comm, cudaEventDisableTiming));
     BT_CUDA(cudaEventCreateWithFlags(&G.ev_main, cudaEventDisableTiming));
+    BT_CUDA(cudaEventCreateWithFlags(&G.ev_idx, cudaEventDisableTiming));
     G.totals.assign(nranks, Counters{});
     G.phases.assign(nranks, {});
     G.phase.assign(nranks, "");
@@ -952,6 +1081,7 @@ int bt_grid_destroy(bt_grid* g) {
     }
     if (G.ev_comm) cudaEventDestroy(G.ev_comm);
     if (G.ev_main) cudaEventDestroy(G.ev_main);
+    if (G.ev_idx) cudaEventDestroy(G.ev_idx);
     delete g;
   });
 }

@@ -186,7 +186,10 @@ __global__ void k_block_norms(const double* vals, const int32_t* row_ptr, const 
 void upload_sizes(Mat& m);
 void check_launch(const char* what);
 // implemented in bt_multiply.cu: C += A*B on one rank's stores (throws bt::Error)
-void local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& C, double eps, bt_stats* stats);
+// wait_numeric (optional): the numeric phase waits for this event (B's values
+// may still be in flight while the symbolic passes run).
+void local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& C, double eps, bt_stats* stats,
+                    cudaEvent_t wait_numeric = nullptr);
 
 }  // namespace bt
 

@@ -496,7 +496,8 @@ Plan plan_dmma(int cls, int ktmax) {
 using namespace bt;
 
 // The local multiply C += A*B (one rank's stores); throws bt::Error.
-void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps, bt_stats* stats) {
+void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps, bt_stats* stats,
+                        cudaEvent_t wait_numeric) {
   {
     BT_REQUIRE(A.ctx == &x && B.ctx == &x && Cm.ctx == &x, BT_ERR_INVALID_ARGUMENT,
                "bt_multiply: matrices belong to another context");
@@ -508,6 +509,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     BT_REQUIRE(&Cm != &A && &Cm != &B, BT_ERR_INVALID_ARGUMENT,
                "multiply: C must not alias A or B");
     BT_CUDA(cudaSetDevice(x.device));
+    Trace tr("multiply");
     cudaStream_t st = x.stream;
     const int64_t k0 = x.kernels;
     bt_stats S{};
@@ -607,7 +609,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     BT_CUDA(cudaMemcpyAsync(&h.nprod, prod_base + M, 8, cudaMemcpyDeviceToHost, st));
     BT_CUDA(cudaMemcpyAsync(&h.nvals, val_base + M, 8, cudaMemcpyDeviceToHost, st));
     BT_CUDA(cudaMemcpyAsync(h.tot, tot, sizeof(h.tot), cudaMemcpyDeviceToHost, st));
+    tr.mark("pass1 enqueued");
     BT_CUDA(cudaStreamSynchronize(st));
+    tr.mark("pass1 sync");
     const int64_t nout = h.nout, nprod = h.nprod, nvals = h.nvals;
     S.candidates = static_cast<int64_t>(h.tot[0]);
     S.flops = 2.0 * static_cast<double>(h.tot[1]);
@@ -662,6 +666,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       count_launch(&x);
     }
 
+    tr.mark("pass2 enqueued");
     // ---- numeric phase: one kernel per tile class, classes run concurrently
     DBuf<double> new_vals(std::max<int64_t>(nvals, 64), st);
     if (nout > 0) {
@@ -673,6 +678,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       g.cin = Cm.vals.p;
       g.cout = new_vals.p;
       unsigned long long* counters = cursor + NCLASS;
+      if (wait_numeric) BT_CUDA(cudaStreamWaitEvent(st, wait_numeric, 0));
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[1], st));
       const int ktmax = std::max(1, tiles8(kmax));
       int nclasses = 0;
@@ -729,7 +735,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     Cm.nvals = nvals;
     Cm.nelems = nelems;
     if (x.timing) BT_CUDA(cudaEventRecord(x.ev[3], st));
+    tr.mark("numeric enqueued");
     BT_CUDA(cudaStreamSynchronize(st));
+    tr.mark("final sync");
     if (x.timing) {
       float ms = 0;
       if (nout > 0) {
