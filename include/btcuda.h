@@ -96,7 +96,9 @@ int bt_mat_clear(bt_mat* m);
 int bt_mat_copy(const bt_mat* src, bt_mat* dst);
 /* DistMatrix::put_block / LocalStore::insert (matrix.hpp:167-189, 305-309), batched:
  * n blocks (bi[t], bj[t]) with compact values in listed order.  accumulate = 0
- * replaces an existing block (later entries of the batch win), 1 adds into it. */
+ * replaces an existing block (later entries of the batch win), 1 adds into it.
+ * vals may be host memory (pinned or pageable) or memory of the context's GPU
+ * (used in place, no staging copy). */
 int bt_mat_put_blocks(bt_mat* m, int64_t n, const int64_t* bi, const int64_t* bj,
                       const double* vals, int accumulate);
 /* number of stored blocks and of stored elements (LocalStore::stored_elements) */

@@ -511,10 +511,19 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
     BT_REQUIRE(col.size() < (size_t(1) << 31), BT_ERR_INVALID_ARGUMENT,
                "store exceeds 2^31 blocks");
     tr.mark("plan");
-    // device: stage inputs, build new slab
-    DBuf<double> d_in(in_total, st);
-    tr.mark("alloc_in");
-    BT_CUDA(cudaMemcpyAsync(d_in.p, vals, sizeof(double) * in_total, cudaMemcpyHostToDevice, st));
+    // device: stage inputs (values already in this GPU's memory are used in
+    // place), build new slab
+    cudaPointerAttributes pa{};
+    const bool on_device = cudaPointerGetAttributes(&pa, vals) == cudaSuccess &&
+                           pa.type == cudaMemoryTypeDevice && pa.device == m.ctx->device;
+    cudaGetLastError();  // clear a possible "invalid value" from unregistered host memory
+    DBuf<double> d_in;
+    const double* src_vals = vals;
+    if (!on_device) {
+      d_in.alloc(in_total, st);
+      BT_CUDA(cudaMemcpyAsync(d_in.p, vals, sizeof(double) * in_total, cudaMemcpyHostToDevice, st));
+      src_vals = d_in.p;
+    }
     tr.mark("h2d_enqueue");
     const int64_t nout = static_cast<int64_t>(col.size());
     DBuf<double> new_vals(std::max<int64_t>(nv, 2), st);
@@ -525,7 +534,7 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
     auto d_iptr = upload(inp_ptr, st);
     auto d_isrc = upload(inp_src, st);
     k_apply_put<<<static_cast<unsigned>(nout), 128, 0, st>>>(
-        new_vals.p, d_off.p, d_dims.p, m.vals.p, d_old.p, d_in.p, d_iptr.p, d_isrc.p, nout);
+        new_vals.p, d_off.p, d_dims.p, m.vals.p, d_old.p, src_vals, d_iptr.p, d_isrc.p, nout);
     check_launch("apply_put");
     count_launch(m.ctx);
     tr.mark("kernel_enqueue");
