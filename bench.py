@@ -37,6 +37,9 @@ sys.path.insert(0, ROOT)
 NB, BS, OCC = 400, 23, 0.10
 SEED_A, SEED_B = 1001, 1002
 FP64_PEAK_TFLOPS = 37.1   # measured: tools/microbench/fp64_peak.cu on B200 (profiles/)
+# dram__bytes_read.sum + dram__bytes_write.sum of one k_smm_dmma launch on this
+# workload, from `ncu --set full` (profiles/r01_ncu_dmma_v4_raw.csv): 1.045 GB + 0.701 GB
+NCU_TRAFFIC_BYTES = 1.746e9
 
 
 # --------------------------------------------------------------- inputs
@@ -300,6 +303,8 @@ def main():
 
     # ---- dominant kernel roofline (small-GEMM numeric phase, live CUDA events)
     kn_ms = float(np.mean(ms_numeric))
+    c_el = c.info()[1] if world == 1 else c.local(rank).info()[1]
+    alg_bytes = 8.0 * (av.size + bv.size * world + c_el) + 12.0 * (len(abi) + len(bbi) * world)
     achieved = flops_step / (kn_ms * 1e-3) / 1e12
 
     # ---- e2e through the public API with host buffers (rank-local)
@@ -365,8 +370,12 @@ def main():
             "roofline": {
                 "bound": "tensor", "achieved": round(achieved, 3),
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
-                "kernel": "k_smm_dmma<3,3,4> (FP64 DMMA 8x8x4 small-GEMM)",
+                "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
+                "traffic": NCU_TRAFFIC_BYTES if world == 1 else None,
+                "traffic_note": "DRAM bytes per launch (ncu); algorithmic bytes "
+                                f"{alg_bytes / 1e9:.3f} GB (8*(|A|+|B|+|C|) T8 slabs + index)",
+                "kernel": "k_smm_dmma<3,3,4,1> (FP64 DMMA 8x8x4 small-GEMM, T8 tiles, "
+                          "bulk-async staged)",
                 "peak_source": "measured FP64 DMMA/DFMA peak on B200 "
                                "(profiles/fp64_peak_r01.txt)",
                 "step_share": round(kn_ms / ms_local, 3),

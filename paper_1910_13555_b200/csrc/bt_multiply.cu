@@ -80,7 +80,8 @@ struct RowArgs {
 // prefix), so all global loads of a chunk are independent (no per-k latency
 // chain).
 constexpr int kChunkA = 256;   // A entries staged per chunk (= blockDim)
-constexpr int kPairCap = 4096; // pairs staged per emission step (k_row_fill)
+constexpr int kPairCap = 2048; // pairs staged per emission window (k_row_fill)
+constexpr int kPairPT = kPairCap / kChunkA;  // pairs per thread in the window sort
 
 struct RowChunk {  // shared-memory staging of up to kChunkA A entries
   int32_t k[kChunkA];
@@ -254,8 +255,11 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   int32_t* cur = reinterpret_cast<int32_t*>(sm + g.ncols);  // product cursor
   uint32_t* bits = sm + 2 * g.ncols;                         // touched columns
   __shared__ RowChunk rc;
-  __shared__ int32_t s_j[kPairCap];  // column of staged pair (-1: filtered out)
-  __shared__ int32_t s_bu[kPairCap]; // B tile offset of staged pair
+  __shared__ int32_t s_bu[kPairCap];  // B tile offset of staged pair
+  __shared__ int16_t s_l[kPairCap];   // local A entry of staged pair
+  __shared__ uint32_t s_key[kPairCap];  // sorted (column, slot) keys
+  using Sort = cub::BlockRadixSort<uint32_t, kChunkA, kPairPT>;
+  __shared__ typename Sort::TempStorage sort_tmp;
   __shared__ unsigned long long cls_n[NCLASS], cls_at[NCLASS];
   const int64_t i = blockIdx.x;
   if (threadIdx.x < NCLASS) cls_n[threadIdx.x] = 0;
@@ -336,34 +340,101 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
     const int n = min(kChunkA, a1 - c0);
     const int64_t T = stage_chunk(g, c0, a1, rc);
-    // windows of <= kPairCap consecutive pairs (windows may split an A entry)
-    for (int64_t w0 = 0; w0 < T; w0 += kPairCap) {
-      const int64_t w1 = min(T, w0 + kPairCap);
-      for (int64_t t = w0 + threadIdx.x; t < w1; t += blockDim.x) {
-        const int l = find_entry(rc, n, static_cast<int32_t>(t));
-        const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
-        const bool keep = keep_product(g.na, g.nb, c0 + l, f, g.eps);
-        s_j[t - w0] = keep ? g.b_col[f] : -1;
-        s_bu[t - w0] = static_cast<int32_t>(g.b_off[f] >> 6);
-      }
-      __syncthreads();
-      // ordered emission: one A entry (one k) at a time
-      const int l_first = find_entry(rc, n, static_cast<int32_t>(w0));
-      const int l_last = find_entry(rc, n, static_cast<int32_t>(w1 - 1));
-      for (int l = l_first; l <= l_last; ++l) {
-        const int32_t e = c0 + l;
-        const int kc = (g.k_sz[rc.k[l]] + 3) >> 2;
-        const int au = static_cast<int>(g.a_off[e] >> 6);
-        const int64_t t0 = max(w0, static_cast<int64_t>(rc.pref[l]));
-        const int64_t t1 = min(w1, static_cast<int64_t>(rc.pref[l + 1]));
-        for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-          const int32_t j = s_j[t - w0];
-          if (j < 0) continue;
-          const int32_t p = cur[j]++;  // one pair per column per k: race free
-          g.desc[pbase + p] = make_int4(au, s_bu[t - w0], kc, 0);
+    // Windows of <= kPairCap consecutive pairs (k ascending).  Inside a window
+    // the kept pairs are sorted by (column, pair index) -- pair index order is
+    // k order -- so every pair's slot is cur[j] + its rank in the column's run:
+    // products stay in ascending k per C block without a step per k.
+    if (n <= 48) {
+      // few A entries (short rows): one k at a time, pairs staged per window
+      for (int64_t w0 = 0; w0 < T; w0 += kPairCap) {
+        const int64_t w1 = min(T, w0 + kPairCap);
+        for (int64_t t = w0 + threadIdx.x; t < w1; t += blockDim.x) {
+          const int slot = static_cast<int>(t - w0);
+          const int l = find_entry(rc, n, static_cast<int32_t>(t));
+          const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
+          const bool keep = keep_product(g.na, g.nb, c0 + l, f, g.eps);
+          s_key[slot] = keep ? static_cast<uint32_t>(g.b_col[f]) : 0xffffffffu;
+          s_bu[slot] = static_cast<int32_t>(g.b_off[f] >> 6);
         }
         __syncthreads();
+        const int l_first = find_entry(rc, n, static_cast<int32_t>(w0));
+        const int l_last = find_entry(rc, n, static_cast<int32_t>(w1 - 1));
+        for (int l = l_first; l <= l_last; ++l) {
+          const int32_t e = c0 + l;
+          const int kc = (g.k_sz[rc.k[l]] + 3) >> 2;
+          const int au = static_cast<int>(g.a_off[e] >> 6);
+          const int64_t t0 = max(w0, static_cast<int64_t>(rc.pref[l]));
+          const int64_t t1 = min(w1, static_cast<int64_t>(rc.pref[l + 1]));
+          for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+            const uint32_t j = s_key[t - w0];
+            if (j == 0xffffffffu) continue;
+            const int32_t p = cur[j]++;  // one pair per column per k: race free
+            g.desc[pbase + p] = make_int4(au, s_bu[t - w0], kc, 0);
+          }
+          __syncthreads();
+        }
       }
+      continue;
+    }
+    for (int64_t w0 = 0; w0 < T; w0 += kPairCap) {
+      const int64_t w1 = min(T, w0 + kPairCap);
+      uint32_t keys[kPairPT];
+#pragma unroll
+      for (int u = 0; u < kPairPT; ++u) {
+        const int slot = threadIdx.x * kPairPT + u;
+        const int64_t t = w0 + slot;
+        keys[u] = 0xffffffffu;
+        if (t < w1) {
+          const int l = find_entry(rc, n, static_cast<int32_t>(t));
+          const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
+          if (keep_product(g.na, g.nb, c0 + l, f, g.eps)) {
+            keys[u] = (static_cast<uint32_t>(g.b_col[f]) << 11) | static_cast<uint32_t>(slot);
+            s_bu[slot] = static_cast<int32_t>(g.b_off[f] >> 6);
+            s_l[slot] = static_cast<int16_t>(l);
+          }
+        }
+      }
+      Sort(sort_tmp).Sort(keys);  // blocked arrangement: thread owns ranks [tid*PT, ...)
+#pragma unroll
+      for (int u = 0; u < kPairPT; ++u) s_key[threadIdx.x * kPairPT + u] = keys[u];
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < kPairPT; ++u) {
+        const uint32_t key = keys[u];
+        if (key == 0xffffffffu) continue;
+        const int q = threadIdx.x * kPairPT + u;
+        const uint32_t jkey = key >> 11;
+        // first rank of this column's run
+        int lo = 0, hi = q;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if ((s_key[mid] >> 11) < jkey) lo = mid + 1; else hi = mid;
+        }
+        const int slot = static_cast<int>(key & 0x7ffu);
+        const int l = s_l[slot];
+        const int32_t e = c0 + l;
+        const int kc = (g.k_sz[rc.k[l]] + 3) >> 2;
+        const int32_t p = cur[jkey] + (q - lo);
+        g.desc[pbase + p] = make_int4(static_cast<int>(g.a_off[e] >> 6), s_bu[slot], kc, 0);
+      }
+      __syncthreads();
+      // advance the column cursors by the run lengths (run ends do it)
+#pragma unroll
+      for (int u = 0; u < kPairPT; ++u) {
+        const int q = threadIdx.x * kPairPT + u;
+        const uint32_t key = s_key[q];
+        if (key == 0xffffffffu) continue;
+        const bool run_end = q + 1 == kPairCap || (s_key[q + 1] >> 11) != (key >> 11);
+        if (run_end) {
+          int lo = 0, hi = q;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((s_key[mid] >> 11) < (key >> 11)) lo = mid + 1; else hi = mid;
+          }
+          cur[key >> 11] += q - lo + 1;
+        }
+      }
+      __syncthreads();
     }
   }
 }
