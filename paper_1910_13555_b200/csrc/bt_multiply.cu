@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
             const uint32_t j = s_key[t - w0];
             if (j == 0xffffffffu) continue;
             const int32_t p = cur[j]++;  // one pair per column per k: race free
-            g.desc[pbase + p] = make_int4(au, s_bu[t - w0], kc, 0);
+            g.desc[pbase + p] = make_int4(au, s_bu[t - w0], kc, rc.k[l]);
           }
           __syncthreads();
         }
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         const int32_t e = c0 + l;
         const int kc = (g.k_sz[rc.k[l]] + 3) >> 2;
         const int32_t p = cur[jkey] + (q - lo);
-        g.desc[pbase + p] = make_int4(static_cast<int>(g.a_off[e] >> 6), s_bu[slot], kc, 0);
+        g.desc[pbase + p] = make_int4(static_cast<int>(g.a_off[e] >> 6), s_bu[slot], kc, rc.k[l]);
       }
       __syncthreads();
       // advance the column cursors by the run lengths (run ends do it)
@@ -436,6 +436,36 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       }
       __syncthreads();
     }
+  }
+}
+
+// K-panel work items (L2 blocking of long product chains):
+// item t of panel p covers the products of base item t whose k block lies in
+// [kb[p], kb[p+1]) -- a sub-range, products being in ascending k.  Panel 0
+// initialises C_out from C_in; later panels accumulate in place (cin = c_out);
+// an in-place item without products is skipped by the kernel.
+__global__ void k_panel_items(const Item* __restrict__ base, int64_t nitems,
+                              const Desc* __restrict__ desc, const int32_t* __restrict__ kb,
+                              int npanels, Item* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nitems) return;
+  const Item it = base[t];
+  const int64_t p0 = it.p0r8 & ((int64_t(1) << 48) - 1);
+  const int64_t r8 = it.p0r8 >> 48;
+  int64_t lo = p0;
+  for (int p = 0; p < npanels; ++p) {
+    // first product with k >= kb[p+1]
+    int64_t a = lo, b = p0 + it.np;
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (desc[mid].w < kb[p + 1]) a = mid + 1; else b = mid;
+    }
+    Item q = it;
+    q.p0r8 = lo | (r8 << 48);
+    q.np = static_cast<int32_t>(a - lo);
+    if (p > 0) q.cin_off = it.c_off;
+    out[p * nitems + t] = q;
+    lo = a;
   }
 }
 
@@ -749,8 +779,47 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       g.cin = Cm.vals.p;
       g.cout = new_vals.p;
       unsigned long long* counters = cursor + NCLASS;
+      // K panels: when the operands are far larger than L2, C is comparatively
+      // small and product chains are long (the case-1 regime: S_C << S_A, S_B),
+      // the numeric phase walks K in panels whose A/B slices fit L2 and
+      // accumulates C in place between panels
+      const double ab_bytes = 8.0 * static_cast<double>(A.nvals + B.nvals);
+      const double c_bytes = 8.0 * static_cast<double>(nvals);
+      int npanels = 1;
+      if (ab_bytes > 2.0 * 126e6 && nitems > 0) {
+        const double per_tile = static_cast<double>(nprod) / static_cast<double>(nitems);
+        int p = static_cast<int>(std::ceil(ab_bytes / 60e6));
+        p = std::min(p, static_cast<int>(per_tile / 4));          // >= ~4 products/panel
+        p = std::min(p, static_cast<int>(0.5 * ab_bytes / (2.0 * c_bytes)));  // C traffic
+        p = std::min(p, 32);
+        npanels = std::max(1, p);
+      }
+      if (nitems > 0) npanels = std::min(64, std::max(1, env_int("BT_KPANELS", npanels)));
+      if (env_int("BT_TRACE", 0))
+        fprintf(stderr, "[bt] numeric: %lld items, %lld products, %d K panel(s)\n",
+                static_cast<long long>(nitems), static_cast<long long>(nprod), npanels);
+      Item* pitems = items;
+      if (npanels > 1) {
+        std::vector<int32_t> kb(npanels + 1);
+        for (int q = 0; q <= npanels; ++q)
+          kb[q] = static_cast<int32_t>((A.nbc * q) / npanels);
+        kb[npanels] = INT32_MAX;
+        int32_t* d_kb = x.ws<int32_t>(20, npanels + 1);
+        BT_CUDA(cudaMemcpyAsync(d_kb, kb.data(), 4 * (npanels + 1), cudaMemcpyHostToDevice, st));
+        pitems = x.ws<Item>(19, static_cast<size_t>(npanels) * nitems);
+        k_panel_items<<<blocks_for(nitems, 256), 256, 0, st>>>(items, nitems, desc, d_kb, npanels,
+                                                               pitems);
+        check_launch("panel_items");
+        count_launch(&x);
+      }
       if (wait_numeric) BT_CUDA(cudaStreamWaitEvent(st, wait_numeric, 0));
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[1], st));
+      for (int panel = 0; panel < npanels; ++panel) {
+      g.items = pitems + static_cast<int64_t>(panel) * nitems;
+      if (panel > 0) {  // later panels accumulate into C_out in place
+        g.cin = g.cout;
+        BT_CUDA(cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * NCLASS, st));
+      }
       const int ktmax = std::max(1, tiles8(kmax));
       int nclasses = 0;
       for (int q = 0; q < NCLASS; ++q) nclasses += ibound[q + 1] > ibound[q];
@@ -794,6 +863,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
           BT_CUDA(cudaEventRecord(x.ev_join[a], x.aux[a]));
           BT_CUDA(cudaStreamWaitEvent(st, x.ev_join[a], 0));
         }
+      }  // panels
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[2], st));
     }
 

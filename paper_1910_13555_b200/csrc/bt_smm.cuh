@@ -240,6 +240,12 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
   while (qh < qt) {
     const Item it = q_items[qh % QN];
     const int mt = (it.rows + 7) >> 3;  // 8-row tiles present in this C tile
+    if (it.np == 0 && it.cin_off == it.c_off && g.cin == g.cout) {  // in-place, no products
+      ++qh;
+      top_up();
+      __syncwarp();
+      continue;
+    }
     double acc[TMT][TNT][2];
 #pragma unroll
     for (int tm = 0; tm < TMT; ++tm)

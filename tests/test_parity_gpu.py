@@ -93,3 +93,22 @@ def test_config1_pattern_and_values(oracle, ctx):
     st = multiply_local(ctx, a, b, c)
     assert st["products"] == nprod and st["flops"] == flops
     assert_parity(from_store(c), want)
+
+
+@pytest.mark.parametrize("npanels", [2, 3, 7])
+def test_k_panels(oracle, ctx, monkeypatch, npanels):
+    """K-panel L2 blocking (forced through BT_KPANELS) is result-identical:
+    panel 0 starts from C_in, later panels accumulate in place; rows whose
+    products all fall in one panel leave the other panels as no-ops."""
+    monkeypatch.setenv("BT_KPANELS", str(npanels))
+    rng = np.random.default_rng(npanels)
+    sizes = np.array([5, 13, 23, 32, 40], np.int32)[rng.integers(0, 5, 30)]
+    ksz = np.array([4, 20, 23], np.int32)[rng.integers(0, 3, 50)]
+    A, B, Cin = _case(oracle, 300 + npanels, sizes, ksz, sizes, 0.3, 0.3, 0.2)
+    for eps in (0.0, 1e-3):
+        want, nprod, _ = oracle.multiply(A, B, Cin, eps)
+        a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+        from paper_1910_13555_b200.store import multiply_local
+        st = multiply_local(ctx, a, b, c, eps)
+        assert st["products"] == nprod
+        assert_parity(from_store(c), want)
