@@ -103,6 +103,13 @@ struct Ctx {
   void* nccl = nullptr; // ncclComm_t when nranks > 1
   DBuf<unsigned char> scratch;  // CUB temp storage, reused
   void* pinned = nullptr;       // small pinned host staging for scalar readbacks
+  // Grow-only pinned host staging for index uploads: one packed H2D per call
+  // instead of several pageable copies.  stage_ev marks the last copy that read
+  // it; host_stage() waits for it before handing the buffer out again.
+  unsigned char* hstage = nullptr;
+  size_t hstage_cap = 0;
+  cudaEvent_t stage_ev = nullptr;
+  unsigned char* host_stage(size_t bytes);
   bool timing = false;          // record CUDA events around multiply kernels
   static constexpr int kAux = 4;  // side streams: concurrent per-class numeric kernels
   cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};
@@ -112,7 +119,7 @@ struct Ctx {
   void* ensure_scratch(size_t bytes);
   // Grow-only per-slot workspace for call-local temporaries (no allocator calls
   // in steady state).  Valid until the next use of the same slot.
-  DBuf<unsigned char> ws_slots[24];
+  DBuf<unsigned char> ws_slots[28];
   template <class T>
   T* ws(int slot, size_t count) {
     const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
@@ -185,6 +192,17 @@ __global__ void k_block_norms(const double* vals, const int32_t* row_ptr, const 
                               int64_t nbr, double* out, int64_t nblk);
 void upload_sizes(Mat& m);
 void check_launch(const char* what);
+// Device-usable alias of a host pointer when it is page-locked and mapped
+// (cudaHostAlloc / cudaHostRegister under UVA), else nullptr.  Kernels read or
+// write such buffers directly over PCIe (no staging copy).
+void* mapped_host_alias(const void* p);
+// Packs `n` host arrays into the pinned stage (one host pass) and enqueues
+// their H2D copies to dst[t] on the context stream (no pageable copies).
+struct HostPart {
+  const void* src;
+  size_t bytes;
+};
+void upload_parts(Ctx& x, const HostPart* parts, int n, void* const* dst);
 // implemented in bt_multiply.cu: C += A*B on one rank's stores (throws bt::Error)
 // wait_numeric (optional): the numeric phase waits for this event (B's values
 // may still be in flight while the symbolic passes run).
