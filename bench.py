@@ -22,6 +22,7 @@ Impls:
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -264,19 +265,23 @@ def main():
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    for _ in range(args.warmup):
-        st = step(c)
-    ctx.sync()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-
-    k_before = ctx.kernel_count
+    # the clock sampler starts BEFORE the warm-up: its start-up pause idles the
+    # GPU, so the warm-up steps bring the clocks back up before the timed steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     ms_numeric = []
     stats = []
+    gc.disable()   # no collector pauses between the host-synchronous API calls
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            st = step(c)
+        ctx.sync()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        k_before = ctx.kernel_count
         for s in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.zero_()                       # L2 flush, outside the timed events
@@ -287,10 +292,15 @@ def main():
             ms_numeric.append(st["ms_numeric"])
             stats.append(st)
         torch.cuda.synchronize()
+    gc.enable()
     if world > 1:
         dist.barrier()
     kernels = ctx.kernel_count - k_before
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    if os.environ.get("BT_BENCH_DEBUG"):
+        print(f"[rank {rank}] step_ms {np.round(step_ms, 3).tolist()} multiply_ms "
+              f"{[round(x['ms_total'], 3) for x in stats]} numeric_ms "
+              f"{[round(x['ms_numeric'], 3) for x in stats]}", file=sys.stderr, flush=True)
     ms_local = float(np.mean(step_ms))
     ms = ms_local
     if world > 1:

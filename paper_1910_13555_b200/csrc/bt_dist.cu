@@ -271,6 +271,9 @@ struct Grid {
   std::unique_ptr<bt_mat> gather_full;
   std::vector<DBuf<int32_t>> gather_rps;
   DBuf<int64_t> gather_sizes;
+  DBuf<int32_t> gather_idx;    // P packed index segments (allgather path)
+  DBuf<int32_t> gather_rdist;  // row -> owning rank of the gathered slabs
+  std::vector<int32_t> gather_rdist_h;
   bool is_local(int r) const { return r >= first && r < first + nlocal; }
   void set_phase(const std::string& p) {
     for (int r = first; r < first + nlocal; ++r) phase[r] = p;
@@ -823,6 +826,124 @@ cudaEvent_t gather_rows_nccl(Grid& g, const Mat& mine, const std::vector<int32_t
   return g.ev_comm;
 }
 
+// Assembles the gathered slabs' index into one store (allgather layout): rank
+// q's segment holds row_ptr (dense over all rows) | col | off, so the global
+// row pointer is the sum of the ranks' row pointers, and row i's entries are
+// those of its owner p = rdist[i], value offsets shifted by p * maxv.  One warp
+// per block row.
+__global__ void k_assemble_gathered(const int32_t* __restrict__ gidx, int64_t seg, int64_t colb,
+                                    int64_t offb, int P, const int32_t* __restrict__ rdist,
+                                    int64_t nbr, int64_t maxv, int32_t* __restrict__ rp,
+                                    int32_t* __restrict__ col, int64_t* __restrict__ off) {
+  const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i > nbr) return;
+  int32_t dst = 0;
+  for (int q = 0; q < P; ++q) dst += gidx[q * seg + i];
+  if (lane == 0) rp[i] = dst;
+  if (i == nbr) return;
+  const int p = rdist[i];
+  const int32_t* s = gidx + p * seg;
+  const int32_t e0 = s[i], n = s[i + 1] - e0;
+  const int32_t* sc = s + colb;
+  const int64_t* so = reinterpret_cast<const int64_t*>(s + offb);
+  const int64_t shift = static_cast<int64_t>(p) * maxv;
+  for (int t = lane; t < n; t += 32) {
+    col[dst + t] = sc[e0 + t];
+    off[dst + t] = so[e0 + t] + shift;
+  }
+}
+
+// All-gather of row slabs into one store with two in-place ncclAllGather calls
+// (every rank of the communicator takes part): the packed index (row_ptr | col
+// | off, padded to the largest slab) and the T8 values (padded likewise).  One
+// size round first (the counts NCCL needs), then both gathers are enqueued on
+// the comm stream at once; the index is assembled by one kernel on the main
+// stream as soon as it lands, while the values keep streaming.  Returns the
+// event recorded when the values have landed.
+cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<int32_t>& rdist,
+                                  int nprocs, Mat& full) {
+  Ctx& x = *g.ctx;
+  Trace tr("gather");
+  ncclComm_t comm = static_cast<ncclComm_t>(x.nccl);
+  const int me = g.first;
+  cudaStream_t cs = g.comm;
+  auto grow = [&](auto& buf, size_t n) {
+    if (buf.n < n) buf.alloc(n + n / 8, x.stream);
+  };
+  grow(g.gather_sizes, static_cast<size_t>(3 * nprocs));
+  DBuf<int64_t>& dsz = g.gather_sizes;
+  int64_t* h = reinterpret_cast<int64_t*>(x.pinned) + 64;
+  h[0] = mine.nblk;
+  h[1] = mine.nvals;
+  h[2] = mine.nelems;
+  BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
+  BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
+  BT_CUDA(cudaMemcpyAsync(dsz.p + 3 * me, h, 24, cudaMemcpyHostToDevice, cs));
+  ncclResult_t r = ncclAllGather(dsz.p + 3 * me, dsz.p, 3, ncclInt64, comm, cs);
+  BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL size gather: ") + ncclGetErrorString(r));
+  BT_CUDA(cudaMemcpyAsync(h + 8, dsz.p, 24 * nprocs, cudaMemcpyDeviceToHost, cs));
+  // the row -> rank map (host -> device only when it changes)
+  if (g.gather_rdist_h != rdist) {
+    g.gather_rdist_h = rdist;
+    grow(g.gather_rdist, rdist.size());
+    BT_CUDA(cudaMemcpyAsync(g.gather_rdist.p, g.gather_rdist_h.data(), 4 * rdist.size(),
+                            cudaMemcpyHostToDevice, x.stream));
+  }
+  BT_CUDA(cudaStreamSynchronize(cs));
+  tr.mark("sizes");
+  int64_t nblk = 0, maxb = 0, maxv = 0, nel = 0;
+  for (int p = 0; p < nprocs; ++p) {
+    nblk += h[8 + 3 * p];
+    maxb = std::max(maxb, h[8 + 3 * p]);
+    maxv = std::max(maxv, h[8 + 3 * p + 1]);
+    nel += h[8 + 3 * p + 2];
+  }
+  const int64_t nbr = full.nbr;
+  const int64_t colb = pad2(nbr + 1);     // int32 words: row_ptr region (even)
+  const int64_t offb = colb + pad2(maxb); // col region (even) -> off 8-byte aligned
+  const int64_t seg = offb + 2 * maxb;
+  grow(g.gather_idx, static_cast<size_t>(seg * nprocs));
+  grow(full.row_ptr, static_cast<size_t>(nbr + 1));
+  grow(full.col, static_cast<size_t>(std::max<int64_t>(nblk, 1)));
+  grow(full.off, static_cast<size_t>(std::max<int64_t>(nblk, 1)));
+  grow(full.vals, static_cast<size_t>(std::max<int64_t>(maxv * nprocs, 64)));
+  full.nblk = nblk;
+  full.nvals = maxv * nprocs;
+  full.nelems = nel;
+  BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
+  BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
+  int32_t* mseg = g.gather_idx.p + seg * me;
+  BT_CUDA(cudaMemcpyAsync(mseg, mine.row_ptr.p, 4 * (nbr + 1), cudaMemcpyDeviceToDevice, cs));
+  if (mine.nblk) {
+    BT_CUDA(cudaMemcpyAsync(mseg + colb, mine.col.p, 4 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
+    BT_CUDA(cudaMemcpyAsync(mseg + offb, mine.off.p, 8 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
+  }
+  r = ncclAllGather(mseg, g.gather_idx.p, seg, ncclInt32, comm, cs);
+  BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL index gather: ") + ncclGetErrorString(r));
+  BT_CUDA(cudaEventRecord(g.ev_idx, cs));
+  if (maxv) {
+    if (mine.nvals)
+      BT_CUDA(cudaMemcpyAsync(full.vals.p + maxv * me, mine.vals.p, 8 * mine.nvals,
+                              cudaMemcpyDeviceToDevice, cs));
+    r = ncclAllGather(full.vals.p + maxv * me, full.vals.p, maxv, ncclFloat64, comm, cs);
+    BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL,
+               std::string("NCCL value gather: ") + ncclGetErrorString(r));
+  }
+  BT_CUDA(cudaEventRecord(g.ev_comm, cs));
+  tr.mark("enqueue rounds");
+  BT_CUDA(cudaStreamWaitEvent(x.stream, g.ev_idx, 0));
+  k_assemble_gathered<<<nb((nbr + 1) * 32, 256), 256, 0, x.stream>>>(
+      g.gather_idx.p, seg, colb, offb, nprocs, g.gather_rdist.p, nbr, maxv, full.row_ptr.p,
+      full.col.p, full.off.p);
+  check_launch("assemble_gathered");
+  count_launch(&x);
+  tr.mark("assemble");
+  g.charge_send(me, (nprocs - 1) * mine.nelems, (nprocs - 1) * 4 * mine.nblk);
+  g.charge_recv(me, nel - mine.nelems, 4 * (nblk - mine.nblk));
+  return g.ev_comm;
+}
+
 }  // namespace
 
 // multiply_cannon (multiply_cannon.hpp:62-118)
@@ -962,7 +1083,11 @@ void case2(const DMat& a, const DMat& b, DMat& c, int nprocs, int gather, double
     if (!g.gather_full || g.gather_full->impl.h_rsz != b.rsz || g.gather_full->impl.h_csz != b.csz)
       g.gather_full = new_store(g.ctx, b.rsz, b.csz);
     Mat& full = g.gather_full->impl;
-    cudaEvent_t vals_ready = gather_rows_nccl(g, bl.view->store(r), ks, nprocs, full);
+    // every rank of the communicator in the gather: two collective calls;
+    // a sub-group: point-to-point rounds
+    cudaEvent_t vals_ready = nprocs == g.P && env_int("BT_GATHER_P2P", 0) == 0
+                                 ? gather_rows_allgather(g, bl.view->store(r), ks, nprocs, full)
+                                 : gather_rows_nccl(g, bl.view->store(r), ks, nprocs, full);
     rank_multiply(g.ctx, al.view->store(r), full, cl->store(r), eps, S, vals_ready);
   } else if (gather) {
     // all-gather of the B slabs

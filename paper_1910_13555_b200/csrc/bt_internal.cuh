@@ -192,6 +192,8 @@ __global__ void k_block_norms(const double* vals, const int32_t* row_ptr, const 
                               int64_t nbr, double* out, int64_t nblk);
 void upload_sizes(Mat& m);
 void check_launch(const char* what);
+// integer environment knob (development / experiments), default when unset
+int env_int(const char* name, int dflt);
 // Device-usable alias of a host pointer when it is page-locked and mapped
 // (cudaHostAlloc / cudaHostRegister under UVA), else nullptr.  Kernels read or
 // write such buffers directly over PCIe (no staging copy).

@@ -24,6 +24,11 @@
 
 namespace bt {
 
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 enum { NCLASS = 17, GENERIC = 16 };
 constexpr uint32_t kCinFlag = 0x80000000u;
 
@@ -519,10 +524,6 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 constexpr int kWarps = 4;
 using KernelFn = void (*)(const NumArgs);
 
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
 
 template <int S>
 KernelFn dmma_kernel_s(int cls) {
