@@ -30,6 +30,11 @@ int env_int(const char* name, int dflt) {
 }
 
 enum { NCLASS = 17, GENERIC = 16 };
+// Work-item segments: (tile class, column band).  Within a class the bands are
+// consecutive, band-major, so the numeric phase sweeps C in column bands and
+// only B(:, band) has to stay resident in L2.
+constexpr int kMaxBands = 8;
+constexpr int NSEG = NCLASS * kMaxBands;
 constexpr uint32_t kCinFlag = 0x80000000u;
 
 // Tile classes: 16 DMMA tile shapes (ceil(m/8) in 1..4 -- taller blocks are cut
@@ -49,6 +54,9 @@ __device__ __forceinline__ bool keep_product(const double* na, const double* nb,
   return !(eps > 0.0) || __dmul_rn(na[e], nb[f]) >= eps;
 }
 
+struct RowArgs;
+__device__ __forceinline__ int band_of(int64_t j, const RowArgs& g);
+
 struct RowArgs {
   const int32_t *a_rp, *a_col, *b_rp, *b_col, *c_rp, *c_col;  // A, B, C_in patterns
   const int64_t *a_off, *b_off, *c_off;                        // T8 offsets (doubles)
@@ -56,13 +64,14 @@ struct RowArgs {
   const double *na, *nb;                                       // block norms (eps > 0)
   double eps;
   int64_t ncols;  // N (block columns of C)
+  int nbands;     // column bands of the numeric sweep (1..kMaxBands)
   bool dmma_ok;
   // pass 1 outputs
   int32_t* row_nnz;
   int64_t* row_prod;
   int64_t* row_vals;
   unsigned long long* totals;       // [0] candidates [1] sum m*n*k [2] stored elements
-  unsigned long long* class_items;  // [NCLASS]
+  unsigned long long* class_items;  // [NSEG]
   // pass 2 inputs/outputs
   const int32_t* out_rp;
   const int64_t* prod_base;  // exclusive scan of row_prod
@@ -75,9 +84,13 @@ struct RowArgs {
   int64_t* out_p0;  // first product per C entry
   Desc* desc;
   // work items, written by the fill pass into per-class segments
-  unsigned long long* class_cursor;  // [NCLASS], initialised to the segment bases
+  unsigned long long* class_cursor;  // [NSEG], initialised to the segment bases
   Item* items;
 };
+
+__device__ __forceinline__ int band_of(int64_t j, const RowArgs& g) {
+  return static_cast<int>((j * g.nbands) / g.ncols);
+}
 
 // Row walk helpers.  A(i,:) x B(k,:) pairs are enumerated load-balanced: the A
 // entries of a chunk are staged in shared memory with the prefix of their B-row
@@ -203,10 +216,10 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
   extern __shared__ uint32_t cnt[];
   uint32_t* bits = cnt + g.ncols;
   int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.ncols + 31) >> 5));
-  __shared__ unsigned long long cls_items[NCLASS];
+  __shared__ unsigned long long cls_items[NSEG];
   __shared__ RowChunk rc;
   const int64_t i = blockIdx.x;
-  if (threadIdx.x < NCLASS) cls_items[threadIdx.x] = 0;
+  for (int t = threadIdx.x; t < NSEG; t += blockDim.x) cls_items[t] = 0;
   unsigned long long cand = 0, mnk = 0;
   row_products(g, i, cnt, bits, rc, &cand, &mnk);
   const int m = g.m_sz[i];
@@ -221,7 +234,8 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
     vals += t8_size(m, n);
     elems += static_cast<long long>(m) * n;
     const int cls = shape_class(m, n, g.dmma_ok);
-    agg_add(&cls_items[cls], cls, static_cast<unsigned long long>(class_tiles(m, cls)));
+    const int seg = cls * kMaxBands + band_of(j, g);
+    agg_add(&cls_items[seg], seg, static_cast<unsigned long long>(class_tiles(m, cls)));
   }
   using BR = cub::BlockReduce<long long, kChunkA>;
   __shared__ typename BR::TempStorage tmp;
@@ -245,8 +259,8 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
     if (t_el) atomicAdd(&g.totals[2], static_cast<unsigned long long>(t_el));
   }
   __syncthreads();
-  if (threadIdx.x < NCLASS && cls_items[threadIdx.x])
-    atomicAdd(&g.class_items[threadIdx.x], cls_items[threadIdx.x]);
+  for (int t = threadIdx.x; t < NSEG; t += blockDim.x)
+    if (cls_items[t]) atomicAdd(&g.class_items[t], cls_items[t]);
 }
 
 // Pass 2: emit C_out row i (columns, T8 offsets, C_in slots, per-block product
@@ -265,9 +279,9 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   __shared__ uint32_t s_key[kPairCap];  // sorted (column, slot) keys
   using Sort = cub::BlockRadixSort<uint32_t, kChunkA, kPairPT>;
   __shared__ typename Sort::TempStorage sort_tmp;
-  __shared__ unsigned long long cls_n[NCLASS], cls_at[NCLASS];
+  __shared__ unsigned long long cls_n[NSEG], cls_at[NSEG];
   const int64_t i = blockIdx.x;
-  if (threadIdx.x < NCLASS) cls_n[threadIdx.x] = 0;
+  for (int t = threadIdx.x; t < NSEG; t += blockDim.x) cls_n[t] = 0;
   row_products(g, i, cnt, bits, rc, nullptr, nullptr);
   const int m = g.m_sz[i];
   const int32_t cbase = g.out_rp[i];
@@ -303,7 +317,8 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         cur[j] = static_cast<int32_t>(run_prod + p_ex);
         cnt[j] = static_cast<uint32_t>(q);
         const int cls = shape_class(m, n, g.dmma_ok);
-        agg_add(&cls_n[cls], cls, static_cast<unsigned long long>(class_tiles(m, cls)));
+        const int seg = cls * kMaxBands + band_of(j, g);
+        agg_add(&cls_n[seg], seg, static_cast<unsigned long long>(class_tiles(m, cls)));
       }
       run_prod += p_tot;
       run_val += v_tot;
@@ -311,9 +326,9 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   }
   __syncthreads();
   // reserve this row's work items in every class segment (one atomic per class)
-  if (threadIdx.x < NCLASS) {
-    const unsigned long long k = cls_n[threadIdx.x];
-    cls_at[threadIdx.x] = k ? atomicAdd(&g.class_cursor[threadIdx.x], k) : 0ull;
+  for (int t = threadIdx.x; t < NSEG; t += blockDim.x) {
+    const unsigned long long k = cls_n[t];
+    cls_at[t] = k ? atomicAdd(&g.class_cursor[t], k) : 0ull;
   }
   __syncthreads();
   // C_in blocks: slot of the matching C_out block
@@ -322,10 +337,12 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   __syncthreads();
   // work items of this row: tall blocks become 32-row tiles
   for (int32_t c = cbase + threadIdx.x; c < g.out_rp[i + 1]; c += blockDim.x) {
-    const int n = g.n_sz[g.out_col[c]];
+    const int j = g.out_col[c];
+    const int n = g.n_sz[j];
     const int cls = shape_class(m, n, g.dmma_ok);
     const int nt = class_tiles(m, cls);
-    const unsigned long long at = agg_add(&cls_at[cls], cls, static_cast<unsigned long long>(nt));
+    const int seg = cls * kMaxBands + band_of(j, g);
+    const unsigned long long at = agg_add(&cls_at[seg], seg, static_cast<unsigned long long>(nt));
     const int64_t cin = g.cin_map[c];
     const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
     for (int q = 0; q < nt; ++q) {
@@ -658,6 +675,19 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.eps = eps;
     ra.ncols = N;
     ra.dmma_ok = dmma_ok;
+    {
+      // column bands: when A and B together overflow a comfortable share of L2
+      // (but are not in the K-panel regime below), sweep C in bands of B
+      // columns so B(:, band) stays L2-resident; A is then streamed once per band
+      const double a_bytes = 8.0 * static_cast<double>(A.nvals);
+      const double b_bytes = 8.0 * static_cast<double>(B.nvals);
+      int nb_ = 1;
+      if (a_bytes + b_bytes > 96e6 && a_bytes + b_bytes <= 2.0 * 126e6)
+        nb_ = static_cast<int>(std::ceil(b_bytes / 40e6));
+      nb_ = env_int("BT_BANDS", nb_);
+      ra.nbands = static_cast<int>(std::min<int64_t>(std::max(1, std::min(nb_, kMaxBands)),
+                                                     std::max<int64_t>(N, 1)));
+    }
 
     // ---- pass 1: sizes (the one host synchronisation)
     DBuf<int32_t> out_rp(M + 1, st);
@@ -666,8 +696,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     int64_t* row_vals = x.ws<int64_t>(2, M + 1);
     int64_t* prod_base = x.ws<int64_t>(3, M + 1);
     int64_t* val_base = x.ws<int64_t>(4, M + 1);
-    unsigned long long* tot = x.ws<unsigned long long>(5, 3 + NCLASS);
-    BT_CUDA(cudaMemsetAsync(tot, 0, sizeof(unsigned long long) * (3 + NCLASS), st));
+    unsigned long long* tot = x.ws<unsigned long long>(5, 3 + NSEG);
+    BT_CUDA(cudaMemsetAsync(tot, 0, sizeof(unsigned long long) * (3 + NSEG), st));
     BT_CUDA(cudaMemsetAsync(row_nnz + M, 0, sizeof(int32_t), st));
     BT_CUDA(cudaMemsetAsync(row_prod + M, 0, sizeof(int64_t), st));
     BT_CUDA(cudaMemsetAsync(row_vals + M, 0, sizeof(int64_t), st));
@@ -703,7 +733,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       int32_t nout;
       int32_t pad;
       int64_t nprod, nvals;
-      unsigned long long tot[3 + NCLASS];
+      unsigned long long tot[3 + NSEG];
     };
     static_assert(sizeof(Sizes) <= 4096, "pinned staging");
     Sizes& h = *reinterpret_cast<Sizes*>(x.pinned);  // pinned: fast readback
@@ -742,16 +772,19 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.out_p0 = out_p0;
     ra.desc = desc;
     // work-item segments per tile class (sizes from pass 1)
+    std::array<int64_t, NSEG + 1> sbound{};
+    for (int q = 0; q < NSEG; ++q) sbound[q + 1] = sbound[q] + static_cast<int64_t>(h.tot[3 + q]);
     std::array<int64_t, NCLASS + 1> ibound{};
-    for (int q = 0; q < NCLASS; ++q) ibound[q + 1] = ibound[q] + static_cast<int64_t>(h.tot[3 + q]);
+    for (int q = 0; q <= NCLASS; ++q) ibound[q] = sbound[q * kMaxBands];
     const int64_t nitems = ibound[NCLASS];
     Item* items = x.ws<Item>(17, nitems);
-    unsigned long long* cursor = x.ws<unsigned long long>(18, 2 * NCLASS);
+    unsigned long long* cursor = x.ws<unsigned long long>(18, NSEG + NCLASS);
     {
+      static_assert(8 * 256 + 8 * (NSEG + NCLASS) <= 4096, "pinned staging");
       unsigned long long* hc = reinterpret_cast<unsigned long long*>(x.pinned) + 256;
-      for (int q = 0; q < NCLASS; ++q) hc[q] = static_cast<unsigned long long>(ibound[q]);
-      for (int q = 0; q < NCLASS; ++q) hc[NCLASS + q] = 0ull;  // ticket counters
-      BT_CUDA(cudaMemcpyAsync(cursor, hc, sizeof(unsigned long long) * 2 * NCLASS,
+      for (int q = 0; q < NSEG; ++q) hc[q] = static_cast<unsigned long long>(sbound[q]);
+      for (int q = 0; q < NCLASS; ++q) hc[NSEG + q] = 0ull;  // ticket counters
+      BT_CUDA(cudaMemcpyAsync(cursor, hc, sizeof(unsigned long long) * (NSEG + NCLASS),
                               cudaMemcpyHostToDevice, st));
     }
     ra.class_cursor = cursor;
@@ -779,7 +812,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       g.bt = B.vals.p;
       g.cin = Cm.vals.p;
       g.cout = new_vals.p;
-      unsigned long long* counters = cursor + NCLASS;
+      unsigned long long* counters = cursor + NSEG;
       // K panels: when the operands are far larger than L2, C is comparatively
       // small and product chains are long (the case-1 regime: S_C << S_A, S_B),
       // the numeric phase walks K in panels whose A/B slices fit L2 and
