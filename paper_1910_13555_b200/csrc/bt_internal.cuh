@@ -115,7 +115,7 @@ struct Ctx {
   cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_join[kAux] = {nullptr, nullptr, nullptr, nullptr};
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   void* ensure_scratch(size_t bytes);
   // Grow-only per-slot workspace for call-local temporaries (no allocator calls
   // in steady state).  Valid until the next use of the same slot.

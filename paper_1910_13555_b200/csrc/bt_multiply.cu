@@ -65,6 +65,8 @@ struct RowArgs {
   double eps;
   int64_t ncols;  // N (block columns of C)
   int nbands;     // column bands of the numeric sweep (1..kMaxBands)
+  int sort_min;   // rows with more A entries per chunk emit by window sort
+  bool colmask;   // k_row_fill has a 64-bit per-column mask array (N <= kMaskCols)
   bool dmma_ok;
   // pass 1 outputs
   int32_t* row_nnz;
@@ -105,6 +107,8 @@ struct RowChunk {  // shared-memory staging of up to kChunkA A entries
   int32_t k[kChunkA];
   int32_t b0[kChunkA];
   int32_t pref[kChunkA + 1];
+  int32_t ksz[kChunkA];  // block size along k
+  int32_t au[kChunkA];   // T8 tile offset of the A block (offset / 64)
 };
 
 // Stage A entries [e0, e0 + kChunkA) of row i; returns the pair count of the chunk.
@@ -120,6 +124,10 @@ __device__ int64_t stage_chunk(const RowArgs& g, int32_t e0, int32_t e1, RowChun
     len = g.b_rp[k + 1] - b0;
     rc.k[threadIdx.x] = k;
     rc.b0[threadIdx.x] = b0;
+    // per-entry constants the emission loops need, loaded once here (in
+    // parallel) so those loops touch shared memory only
+    rc.ksz[threadIdx.x] = g.k_sz[k];
+    rc.au[threadIdx.x] = static_cast<int32_t>(g.a_off[e] >> 6);
   }
   int32_t ex, tot;
   BS(tmp).ExclusiveSum(len, ex, tot);
@@ -167,7 +175,7 @@ __device__ void row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
       if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
       const int32_t j = g.b_col[f];
       if (atomicAdd(&cnt[j], 1u) == 0u) atomicOr(&bits[j >> 5], 1u << (j & 31));
-      if (mnk) *mnk += static_cast<unsigned long long>(g.k_sz[rc.k[l]]) * g.n_sz[j];
+      if (mnk) *mnk += static_cast<unsigned long long>(rc.ksz[l]) * g.n_sz[j];
     }
     __syncthreads();
   }
@@ -362,11 +370,44 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
     const int n = min(kChunkA, a1 - c0);
     const int64_t T = stage_chunk(g, c0, a1, rc);
+    if (g.colmask && n <= 64) {
+      // Rank emission (chunks of <= 64 A entries): bit l of mask[j] marks the
+      // pair (A entry l, column j); a pair's slot in its C block is cur[j] +
+      // the number of lower entries l' < l in that column, i.e. k ascending,
+      // in two parallel sweeps over the pairs -- no step per k.
+      unsigned long long* mask = reinterpret_cast<unsigned long long*>(
+          sm + ((3 * g.ncols + ((g.ncols + 31) >> 5) + 1) & ~int64_t(1)));
+      for (int q = threadIdx.x; q < ntouch; q += blockDim.x) mask[tcol[q]] = 0ull;
+      __syncthreads();
+      for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+        const int l = find_entry(rc, n, static_cast<int32_t>(t));
+        const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
+        if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
+        atomicOr(&mask[g.b_col[f]], 1ull << l);
+      }
+      __syncthreads();
+      for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+        const int l = find_entry(rc, n, static_cast<int32_t>(t));
+        const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
+        if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
+        const int32_t j = g.b_col[f];
+        const int32_t p = cur[j] + __popcll(mask[j] & ((1ull << l) - 1ull));
+        g.desc[pbase + p] = make_int4(rc.au[l], static_cast<int32_t>(g.b_off[f] >> 6),
+                                      (rc.ksz[l] + 3) >> 2, rc.k[l]);
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < ntouch; q += blockDim.x) {
+        const int j = tcol[q];
+        cur[j] += __popcll(mask[j]);
+      }
+      __syncthreads();
+      continue;
+    }
     // Windows of <= kPairCap consecutive pairs (k ascending).  Inside a window
     // the kept pairs are sorted by (column, pair index) -- pair index order is
     // k order -- so every pair's slot is cur[j] + its rank in the column's run:
     // products stay in ascending k per C block without a step per k.
-    if (n <= 48) {
+    if (n <= g.sort_min) {
       // few A entries (short rows): one k at a time, pairs staged per window
       for (int64_t w0 = 0; w0 < T; w0 += kPairCap) {
         const int64_t w1 = min(T, w0 + kPairCap);
@@ -382,9 +423,8 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         const int l_first = find_entry(rc, n, static_cast<int32_t>(w0));
         const int l_last = find_entry(rc, n, static_cast<int32_t>(w1 - 1));
         for (int l = l_first; l <= l_last; ++l) {
-          const int32_t e = c0 + l;
-          const int kc = (g.k_sz[rc.k[l]] + 3) >> 2;
-          const int au = static_cast<int>(g.a_off[e] >> 6);
+          const int kc = (rc.ksz[l] + 3) >> 2;
+          const int au = rc.au[l];
           const int64_t t0 = max(w0, static_cast<int64_t>(rc.pref[l]));
           const int64_t t1 = min(w1, static_cast<int64_t>(rc.pref[l + 1]));
           for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
@@ -434,10 +474,9 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         }
         const int slot = static_cast<int>(key & 0x7ffu);
         const int l = s_l[slot];
-        const int32_t e = c0 + l;
-        const int kc = (g.k_sz[rc.k[l]] + 3) >> 2;
+        const int kc = (rc.ksz[l] + 3) >> 2;
         const int32_t p = cur[jkey] + (q - lo);
-        g.desc[pbase + p] = make_int4(static_cast<int>(g.a_off[e] >> 6), s_bu[slot], kc, rc.k[l]);
+        g.desc[pbase + p] = make_int4(rc.au[l], s_bu[slot], kc, rc.k[l]);
       }
       __syncthreads();
       // advance the column cursors by the run lengths (run ends do it)
@@ -491,6 +530,19 @@ __global__ void k_panel_items(const Item* __restrict__ base, int64_t nitems,
   }
 }
 
+// Work-item segment bases (exclusive scan of the per-segment counts) and zeroed
+// ticket counters, written on the device: no host round trip before the fill.
+__device__ void init_cursors(const unsigned long long* seg_items, unsigned long long* cursor) {
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    for (int q = 0; q < NSEG; ++q) {
+      cursor[q] = run;
+      run += seg_items[q];
+    }
+  }
+  for (int q = threadIdx.x; q < NCLASS; q += blockDim.x) cursor[NSEG + q] = 0ull;
+}
+
 // Exclusive scans of the three per-row arrays in one single-CTA kernel (small M);
 // element M receives the totals.
 __global__ void __launch_bounds__(1024) k_scan_rows(const int32_t* __restrict__ nnz,
@@ -498,7 +550,11 @@ __global__ void __launch_bounds__(1024) k_scan_rows(const int32_t* __restrict__ 
                                                     const int64_t* __restrict__ vals, int64_t M,
                                                     int32_t* __restrict__ rp,
                                                     int64_t* __restrict__ pb,
-                                                    int64_t* __restrict__ vb) {
+                                                    int64_t* __restrict__ vb,
+                                                    const unsigned long long* __restrict__ tot,
+                                                    int ntot,
+                                                    unsigned long long* __restrict__ sizes,
+                                                    unsigned long long* __restrict__ cursor) {
   using BS = cub::BlockScan<long long, 1024>;
   __shared__ typename BS::TempStorage tmp;
   long long r0 = 0, r1 = 0, r2 = 0;
@@ -521,6 +577,29 @@ __global__ void __launch_bounds__(1024) k_scan_rows(const int32_t* __restrict__ 
     r1 += tb;
     r2 += tc;
   }
+  // one contiguous block for the host readback: totals, then the counters
+  if (threadIdx.x == 0) {
+    sizes[0] = static_cast<unsigned long long>(r0);
+    sizes[1] = static_cast<unsigned long long>(r1);
+    sizes[2] = static_cast<unsigned long long>(r2);
+  }
+  for (int t = threadIdx.x; t < ntot; t += blockDim.x) sizes[3 + t] = tot[t];
+  init_cursors(tot + 3, cursor);
+}
+
+// Large-M variant of the readback block (after the CUB scans).
+__global__ void k_pack_sizes(const int32_t* __restrict__ rp, const int64_t* __restrict__ pb,
+                             const int64_t* __restrict__ vb, int64_t M,
+                             const unsigned long long* __restrict__ tot, int ntot,
+                             unsigned long long* __restrict__ sizes,
+                             unsigned long long* __restrict__ cursor) {
+  if (threadIdx.x == 0) {
+    sizes[0] = static_cast<unsigned long long>(rp[M]);
+    sizes[1] = static_cast<unsigned long long>(pb[M]);
+    sizes[2] = static_cast<unsigned long long>(vb[M]);
+  }
+  for (int t = threadIdx.x; t < ntot; t += blockDim.x) sizes[3 + t] = tot[t];
+  init_cursors(tot + 3, cursor);
 }
 
 // ------------------------------------------------------------------- host
@@ -636,7 +715,10 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     if (x.timing) BT_CUDA(cudaEventRecord(x.ev[0], st));
     const int64_t M = Cm.nbr, N = Cm.nbc;
     // fill pass: 3 ints per column (counts, cursors, touched list) + bitmap
-    const size_t row_smem = static_cast<size_t>(N) * 12 + 4 * ((N + 31) / 32);
+    size_t row_smem = static_cast<size_t>(N) * 12 + 4 * ((N + 31) / 32);
+    // the fill pass's rank emission needs 8 more bytes per column
+    const bool colmask = N <= 4096 && env_int("BT_COLMASK", 1);
+    if (colmask) row_smem = 4 * ((3 * N + (N + 31) / 32 + 1) & ~int64_t(1)) + 8 * N;
     BT_REQUIRE(row_smem <= 180 * 1024, BT_ERR_INVALID_ARGUMENT,
                "multiply: more than 15000 block columns per C row is not supported");
 
@@ -675,6 +757,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.eps = eps;
     ra.ncols = N;
     ra.dmma_ok = dmma_ok;
+    ra.sort_min = env_int("BT_SORT_MIN", 48);
+    ra.colmask = colmask;
     {
       // column bands: when A and B together overflow a comfortable share of L2
       // (but are not in the K-panel regime below), sweep C in bands of B
@@ -698,9 +782,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     int64_t* val_base = x.ws<int64_t>(4, M + 1);
     unsigned long long* tot = x.ws<unsigned long long>(5, 3 + NSEG);
     BT_CUDA(cudaMemsetAsync(tot, 0, sizeof(unsigned long long) * (3 + NSEG), st));
-    BT_CUDA(cudaMemsetAsync(row_nnz + M, 0, sizeof(int32_t), st));
-    BT_CUDA(cudaMemsetAsync(row_prod + M, 0, sizeof(int64_t), st));
-    BT_CUDA(cudaMemsetAsync(row_vals + M, 0, sizeof(int64_t), st));
+    unsigned long long* dsizes = x.ws<unsigned long long>(11, 6 + NSEG);
+    unsigned long long* cursor = x.ws<unsigned long long>(18, NSEG + NCLASS);
     ra.row_nnz = row_nnz;
     ra.row_prod = row_prod;
     ra.row_vals = row_vals;
@@ -721,30 +804,35 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     }
     if (M <= 8192) {
       k_scan_rows<<<1, 1024, 0, st>>>(row_nnz, row_prod, row_vals, M, out_rp.p, prod_base,
-                                      val_base);
+                                      val_base, tot, 3 + NSEG, dsizes, cursor);
       check_launch("scan_rows");
       count_launch(&x);
     } else {
+      BT_CUDA(cudaMemsetAsync(row_nnz + M, 0, sizeof(int32_t), st));
+      BT_CUDA(cudaMemsetAsync(row_prod + M, 0, sizeof(int64_t), st));
+      BT_CUDA(cudaMemsetAsync(row_vals + M, 0, sizeof(int64_t), st));
       exclusive_scan(x, row_nnz, out_rp.p, M + 1);
       exclusive_scan(x, row_prod, prod_base, M + 1);
       exclusive_scan(x, row_vals, val_base, M + 1);
+      k_pack_sizes<<<1, 256, 0, st>>>(out_rp.p, prod_base, val_base, M, tot, 3 + NSEG, dsizes,
+                                      cursor);
+      check_launch("pack_sizes");
+      count_launch(&x);
     }
     struct Sizes {
-      int32_t nout;
-      int32_t pad;
-      int64_t nprod, nvals;
+      unsigned long long nout, nprod, nvals;
       unsigned long long tot[3 + NSEG];
     };
-    static_assert(sizeof(Sizes) <= 4096, "pinned staging");
-    Sizes& h = *reinterpret_cast<Sizes*>(x.pinned);  // pinned: fast readback
-    BT_CUDA(cudaMemcpyAsync(&h.nout, out_rp.p + M, 4, cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(&h.nprod, prod_base + M, 8, cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(&h.nvals, val_base + M, 8, cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(h.tot, tot, sizeof(h.tot), cudaMemcpyDeviceToHost, st));
+    static_assert(sizeof(Sizes) <= 2048, "pinned staging");
+    Sizes& h = *reinterpret_cast<Sizes*>(x.pinned);  // pinned: one readback
+    BT_CUDA(cudaMemcpyAsync(&h, dsizes, sizeof(Sizes), cudaMemcpyDeviceToHost, st));
+    const bool phases = x.timing && env_int("BT_PHASES", 0);
+    if (phases) BT_CUDA(cudaEventRecord(x.ev[4], st));
     tr.mark("pass1 enqueued");
     BT_CUDA(cudaStreamSynchronize(st));
     tr.mark("pass1 sync");
-    const int64_t nout = h.nout, nprod = h.nprod, nvals = h.nvals;
+    const int64_t nout = static_cast<int64_t>(h.nout), nprod = static_cast<int64_t>(h.nprod),
+                  nvals = static_cast<int64_t>(h.nvals);
     S.candidates = static_cast<int64_t>(h.tot[0]);
     S.flops = 2.0 * static_cast<double>(h.tot[1]);
     S.products = nprod;
@@ -778,17 +866,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     for (int q = 0; q <= NCLASS; ++q) ibound[q] = sbound[q * kMaxBands];
     const int64_t nitems = ibound[NCLASS];
     Item* items = x.ws<Item>(17, nitems);
-    unsigned long long* cursor = x.ws<unsigned long long>(18, NSEG + NCLASS);
-    {
-      static_assert(8 * 256 + 8 * (NSEG + NCLASS) <= 4096, "pinned staging");
-      unsigned long long* hc = reinterpret_cast<unsigned long long*>(x.pinned) + 256;
-      for (int q = 0; q < NSEG; ++q) hc[q] = static_cast<unsigned long long>(sbound[q]);
-      for (int q = 0; q < NCLASS; ++q) hc[NSEG + q] = 0ull;  // ticket counters
-      BT_CUDA(cudaMemcpyAsync(cursor, hc, sizeof(unsigned long long) * (NSEG + NCLASS),
-                              cudaMemcpyHostToDevice, st));
-    }
     ra.class_cursor = cursor;
     ra.items = items;
+    if (phases) BT_CUDA(cudaEventRecord(x.ev[5], st));
     if (nout > 0) {
       static size_t set2 = 0;
       if (row_smem > set2) {
@@ -846,6 +926,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         check_launch("panel_items");
         count_launch(&x);
       }
+      if (phases) BT_CUDA(cudaEventRecord(x.ev[6], st));
       if (wait_numeric) BT_CUDA(cudaStreamWaitEvent(st, wait_numeric, 0));
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[1], st));
       for (int panel = 0; panel < npanels; ++panel) {
@@ -921,6 +1002,16 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       }
       BT_CUDA(cudaEventElapsedTime(&ms, x.ev[0], x.ev[3]));
       S.ms_total = ms;
+      if (phases && nout > 0) {
+        float a, b, c, d;
+        BT_CUDA(cudaEventElapsedTime(&a, x.ev[0], x.ev[4]));
+        BT_CUDA(cudaEventElapsedTime(&b, x.ev[4], x.ev[5]));
+        BT_CUDA(cudaEventElapsedTime(&c, x.ev[5], x.ev[6]));
+        BT_CUDA(cudaEventElapsedTime(&d, x.ev[6], x.ev[1]));
+        fprintf(stderr, "[bt-phases] pass1+scan %.1f us | host sync gap %.1f us | fill %.1f us | "
+                        "pre-numeric %.1f us | numeric %.1f us | total %.1f us\n",
+                1e3 * a, 1e3 * b, 1e3 * c, 1e3 * d, 1e3 * S.ms_numeric, 1e3 * ms);
+      }
     }
     S.c_blocks_out = nout;
     S.kernels = static_cast<int32_t>(x.kernels - k0);
