@@ -272,6 +272,7 @@ struct Grid {
   std::vector<DBuf<int32_t>> gather_rps;
   DBuf<int64_t> gather_sizes;
   DBuf<int32_t> gather_idx;    // P packed index segments (allgather path)
+  cudaEvent_t phase_ev = nullptr;  // BT_PHASES: recorded at the numeric start
   DBuf<int32_t> gather_rdist;  // row -> owning rank of the gathered slabs
   std::vector<int32_t> gather_rdist_h;
   bool is_local(int r) const { return r >= first && r < first + nlocal; }
@@ -603,9 +604,9 @@ void add_stats(bt_stats& acc, const bt_stats& s) {
 }
 
 void rank_multiply(Ctx* ctx, const Mat& a, const Mat& b, Mat& c, double eps, bt_stats& acc,
-                   cudaEvent_t wait_numeric = nullptr) {
+                   cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr) {
   bt_stats s{};
-  local_multiply(*ctx, a, b, c, eps, &s, wait_numeric);
+  local_multiply(*ctx, a, b, c, eps, &s, wait_numeric, numeric_start);
   add_stats(acc, s);
 }
 
@@ -868,21 +869,27 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
   ncclComm_t comm = static_cast<ncclComm_t>(x.nccl);
   const int me = g.first;
   cudaStream_t cs = g.comm;
+  // BT_PHASES=1: device timeline of the gather (rank 0 prints the previous call's)
+  static cudaEvent_t pev[6] = {};
+  static bool pev_recorded = false;
+  const bool phases = env_int("BT_PHASES", 0) != 0;
+  if (phases && !pev[0])
+    for (auto& e : pev) BT_CUDA(cudaEventCreate(&e));
+  if (phases && me == 0 && pev_recorded) {
+    BT_CUDA(cudaEventSynchronize(pev[5]));
+    float t[5];
+    for (int q = 0; q < 5; ++q) BT_CUDA(cudaEventElapsedTime(&t[q], pev[0], pev[q + 1]));
+    fprintf(stderr, "[bt-gather] sizes %.1f | index %.1f | assembled %.1f | values %.1f | "
+                    "numeric start %.1f us\n", 1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3],
+            1e3 * t[4]);
+  }
   auto grow = [&](auto& buf, size_t n) {
     if (buf.n < n) buf.alloc(n + n / 8, x.stream);
   };
-  grow(g.gather_sizes, static_cast<size_t>(3 * nprocs));
-  DBuf<int64_t>& dsz = g.gather_sizes;
   int64_t* h = reinterpret_cast<int64_t*>(x.pinned) + 64;
   h[0] = mine.nblk;
   h[1] = mine.nvals;
   h[2] = mine.nelems;
-  BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
-  BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
-  BT_CUDA(cudaMemcpyAsync(dsz.p + 3 * me, h, 24, cudaMemcpyHostToDevice, cs));
-  ncclResult_t r = ncclAllGather(dsz.p + 3 * me, dsz.p, 3, ncclInt64, comm, cs);
-  BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL size gather: ") + ncclGetErrorString(r));
-  BT_CUDA(cudaMemcpyAsync(h + 8, dsz.p, 24 * nprocs, cudaMemcpyDeviceToHost, cs));
   // the row -> rank map (host -> device only when it changes)
   if (g.gather_rdist_h != rdist) {
     g.gather_rdist_h = rdist;
@@ -890,20 +897,68 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
     BT_CUDA(cudaMemcpyAsync(g.gather_rdist.p, g.gather_rdist_h.data(), 4 * rdist.size(),
                             cudaMemcpyHostToDevice, x.stream));
   }
-  BT_CUDA(cudaStreamSynchronize(cs));
+  const int64_t nbr = full.nbr;
+  // Index segment capacity.  Default: a size round fixes the exact maximum
+  // first.  BT_GATHER_ONE_ROUND=1: every rank bounds a slab's block count by
+  // its rows x all columns without communication and the index goes out at
+  // once with a 3-word size header in front -- measured slower on 4 B200s
+  // (the padded index round and the later host sync cost more than the size
+  // round saves), kept as an option.
+  std::vector<int64_t> rows_of(nprocs, 0);
+  for (int32_t p : rdist)
+    if (p >= 0 && p < nprocs) ++rows_of[p];
+  const int64_t cap = *std::max_element(rows_of.begin(), rows_of.end()) * full.nbc;
+  const bool one_round = cap * 12 <= (int64_t(64) << 20) && env_int("BT_GATHER_ONE_ROUND", 0) == 1;
+  ncclResult_t r;
+  int64_t maxb;
+  BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
+  if (phases) BT_CUDA(cudaEventRecord(pev[0], x.stream));
+  BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
+  if (one_round) {
+    maxb = cap;
+    if (phases) BT_CUDA(cudaEventRecord(pev[1], cs));
+  } else {
+    grow(g.gather_sizes, static_cast<size_t>(3 * nprocs));
+    DBuf<int64_t>& dsz = g.gather_sizes;
+    BT_CUDA(cudaMemcpyAsync(dsz.p + 3 * me, h, 24, cudaMemcpyHostToDevice, cs));
+    r = ncclAllGather(dsz.p + 3 * me, dsz.p, 3, ncclInt64, comm, cs);
+    if (phases) BT_CUDA(cudaEventRecord(pev[1], cs));
+    BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL,
+               std::string("NCCL size gather: ") + ncclGetErrorString(r));
+    BT_CUDA(cudaMemcpyAsync(h + 8, dsz.p, 24 * nprocs, cudaMemcpyDeviceToHost, cs));
+    BT_CUDA(cudaStreamSynchronize(cs));
+    maxb = 0;
+    for (int p = 0; p < nprocs; ++p) maxb = std::max(maxb, h[8 + 3 * p]);
+  }
   tr.mark("sizes");
-  int64_t nblk = 0, maxb = 0, maxv = 0, nel = 0;
+  // segment (int32 words): header (3 x int64) | row_ptr | col | off
+  const int64_t rpb = 6;
+  const int64_t colb = rpb + pad2(nbr + 1);
+  const int64_t offb = colb + pad2(maxb);
+  const int64_t seg = offb + 2 * maxb;
+  grow(g.gather_idx, static_cast<size_t>(seg * nprocs));
+  int32_t* mseg = g.gather_idx.p + seg * me;
+  BT_CUDA(cudaMemcpyAsync(mseg, h, 24, cudaMemcpyHostToDevice, cs));
+  BT_CUDA(cudaMemcpyAsync(mseg + rpb, mine.row_ptr.p, 4 * (nbr + 1), cudaMemcpyDeviceToDevice, cs));
+  if (mine.nblk) {
+    BT_CUDA(cudaMemcpyAsync(mseg + colb, mine.col.p, 4 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
+    BT_CUDA(cudaMemcpyAsync(mseg + offb, mine.off.p, 8 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
+  }
+  r = ncclAllGather(mseg, g.gather_idx.p, seg, ncclInt32, comm, cs);
+  BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL index gather: ") + ncclGetErrorString(r));
+  BT_CUDA(cudaEventRecord(g.ev_idx, cs));
+  if (one_round) {  // the headers: one strided readback
+    BT_CUDA(cudaMemcpy2DAsync(h + 8, 24, g.gather_idx.p, 4 * seg, 24, nprocs,
+                              cudaMemcpyDeviceToHost, cs));
+    BT_CUDA(cudaStreamSynchronize(cs));
+  }
+  tr.mark("index");
+  int64_t nblk = 0, maxv = 0, nel = 0;
   for (int p = 0; p < nprocs; ++p) {
     nblk += h[8 + 3 * p];
-    maxb = std::max(maxb, h[8 + 3 * p]);
     maxv = std::max(maxv, h[8 + 3 * p + 1]);
     nel += h[8 + 3 * p + 2];
   }
-  const int64_t nbr = full.nbr;
-  const int64_t colb = pad2(nbr + 1);     // int32 words: row_ptr region (even)
-  const int64_t offb = colb + pad2(maxb); // col region (even) -> off 8-byte aligned
-  const int64_t seg = offb + 2 * maxb;
-  grow(g.gather_idx, static_cast<size_t>(seg * nprocs));
   grow(full.row_ptr, static_cast<size_t>(nbr + 1));
   grow(full.col, static_cast<size_t>(std::max<int64_t>(nblk, 1)));
   grow(full.off, static_cast<size_t>(std::max<int64_t>(nblk, 1)));
@@ -913,15 +968,7 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
   full.nelems = nel;
   BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
   BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
-  int32_t* mseg = g.gather_idx.p + seg * me;
-  BT_CUDA(cudaMemcpyAsync(mseg, mine.row_ptr.p, 4 * (nbr + 1), cudaMemcpyDeviceToDevice, cs));
-  if (mine.nblk) {
-    BT_CUDA(cudaMemcpyAsync(mseg + colb, mine.col.p, 4 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
-    BT_CUDA(cudaMemcpyAsync(mseg + offb, mine.off.p, 8 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
-  }
-  r = ncclAllGather(mseg, g.gather_idx.p, seg, ncclInt32, comm, cs);
-  BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL index gather: ") + ncclGetErrorString(r));
-  BT_CUDA(cudaEventRecord(g.ev_idx, cs));
+  if (phases) BT_CUDA(cudaEventRecord(pev[2], cs));
   if (maxv) {
     if (mine.nvals)
       BT_CUDA(cudaMemcpyAsync(full.vals.p + maxv * me, mine.vals.p, 8 * mine.nvals,
@@ -931,13 +978,19 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
                std::string("NCCL value gather: ") + ncclGetErrorString(r));
   }
   BT_CUDA(cudaEventRecord(g.ev_comm, cs));
+  if (phases) BT_CUDA(cudaEventRecord(pev[4], cs));
   tr.mark("enqueue rounds");
   BT_CUDA(cudaStreamWaitEvent(x.stream, g.ev_idx, 0));
   k_assemble_gathered<<<nb((nbr + 1) * 32, 256), 256, 0, x.stream>>>(
-      g.gather_idx.p, seg, colb, offb, nprocs, g.gather_rdist.p, nbr, maxv, full.row_ptr.p,
-      full.col.p, full.off.p);
+      g.gather_idx.p + rpb, seg, colb - rpb, offb - rpb, nprocs, g.gather_rdist.p, nbr, maxv,
+      full.row_ptr.p, full.col.p, full.off.p);
   check_launch("assemble_gathered");
   count_launch(&x);
+  if (phases) {
+    BT_CUDA(cudaEventRecord(pev[3], x.stream));
+    g.phase_ev = pev[5];  // recorded by the multiply when its numeric phase starts
+    pev_recorded = true;
+  }
   tr.mark("assemble");
   g.charge_send(me, (nprocs - 1) * mine.nelems, (nprocs - 1) * 4 * mine.nblk);
   g.charge_recv(me, nel - mine.nelems, 4 * (nblk - mine.nblk));
@@ -1088,7 +1141,8 @@ void case2(const DMat& a, const DMat& b, DMat& c, int nprocs, int gather, double
     cudaEvent_t vals_ready = nprocs == g.P && env_int("BT_GATHER_P2P", 0) == 0
                                  ? gather_rows_allgather(g, bl.view->store(r), ks, nprocs, full)
                                  : gather_rows_nccl(g, bl.view->store(r), ks, nprocs, full);
-    rank_multiply(g.ctx, al.view->store(r), full, cl->store(r), eps, S, vals_ready);
+    rank_multiply(g.ctx, al.view->store(r), full, cl->store(r), eps, S, vals_ready, g.phase_ev);
+    g.phase_ev = nullptr;
   } else if (gather) {
     // all-gather of the B slabs
     std::vector<std::vector<std::unique_ptr<bt_mat>>> got(g.nlocal);

@@ -209,7 +209,7 @@ void upload_parts(Ctx& x, const HostPart* parts, int n, void* const* dst);
 // wait_numeric (optional): the numeric phase waits for this event (B's values
 // may still be in flight while the symbolic passes run).
 void local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& C, double eps, bt_stats* stats,
-                    cudaEvent_t wait_numeric = nullptr);
+                    cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr);
 
 }  // namespace bt
 

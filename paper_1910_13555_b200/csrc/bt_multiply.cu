@@ -695,7 +695,7 @@ using namespace bt;
 
 // The local multiply C += A*B (one rank's stores); throws bt::Error.
 void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps, bt_stats* stats,
-                        cudaEvent_t wait_numeric) {
+                        cudaEvent_t wait_numeric, cudaEvent_t numeric_start) {
   {
     BT_REQUIRE(A.ctx == &x && B.ctx == &x && Cm.ctx == &x, BT_ERR_INVALID_ARGUMENT,
                "bt_multiply: matrices belong to another context");
@@ -928,6 +928,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       }
       if (phases) BT_CUDA(cudaEventRecord(x.ev[6], st));
       if (wait_numeric) BT_CUDA(cudaStreamWaitEvent(st, wait_numeric, 0));
+      if (numeric_start) BT_CUDA(cudaEventRecord(numeric_start, st));
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[1], st));
       for (int panel = 0; panel < npanels; ++panel) {
       g.items = pitems + static_cast<int64_t>(panel) * nitems;
