@@ -39,8 +39,9 @@ NB, BS, OCC = 400, 23, 0.10
 SEED_A, SEED_B = 1001, 1002
 FP64_PEAK_TFLOPS = 37.1   # measured: tools/microbench/fp64_peak.cu on B200 (profiles/)
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_smm_dmma launch on this
-# workload, from `ncu --set full` (profiles/r01_ncu_dmma_v4_raw.csv): 1.045 GB + 0.701 GB
-NCU_TRAFFIC_BYTES = 1.746e9
+# workload, from `ncu --set full` of this bench (profiles/r01b_ncu_dmma_bench_raw.csv):
+# 0.602 GB read + 0.696 GB written (algorithmic: 0.80 GB)
+NCU_TRAFFIC_BYTES = 1.298e9
 
 
 # --------------------------------------------------------------- inputs
