@@ -112,3 +112,78 @@ def test_k_panels(oracle, ctx, monkeypatch, npanels):
         st = multiply_local(ctx, a, b, c, eps)
         assert st["products"] == nprod
         assert_parity(from_store(c), want)
+
+
+@pytest.mark.parametrize("colmask,sort_min", [(1, 48), (0, 48), (0, 0), (0, 100000), (1, 0)])
+def test_emission_paths(oracle, ctx, monkeypatch, colmask, sort_min):
+    """The fill pass's three product-emission paths (rank emission by column
+    masks for chunks of <= 64 A entries, window sort, one step per k) give the
+    same descriptors: rows here have 3 .. 300 A entries (one and two chunks)."""
+    monkeypatch.setenv("BT_COLMASK", str(colmask))
+    monkeypatch.setenv("BT_SORT_MIN", str(sort_min))
+    rng = np.random.default_rng(41)
+    rsz = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 6)]
+    ksz = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 300)]
+    nsz = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 20)]
+    A = _dense_rows(oracle, oracle.random_matrix(901, rsz, ksz, 0.01), rsz, ksz, rng)
+    B = oracle.random_matrix(902, ksz, nsz, 0.3)
+    Cin = oracle.random_matrix(903, rsz, nsz, 0.2)
+    for eps in (0.0, 30.0):
+        want, nprod, _ = oracle.multiply(A, B, Cin, eps)
+        a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+        from paper_1910_13555_b200.store import multiply_local
+        st = multiply_local(ctx, a, b, c, eps)
+        assert st["products"] == nprod
+        assert_parity(from_store(c), want)
+
+
+def _dense_rows(oracle, A, rsz, ksz, rng):
+    """A with rows 0/1/2 at occupancy 1.0/0.5/0.2 over 300 block columns (the
+    remaining rows as drawn): long A rows exercise the multi-chunk paths."""
+    from oracle.oracle import Blocks
+    keep = A.bi >= 3
+    bi, bj = [A.bi[keep]], [A.bj[keep]]
+    for i, occ in ((0, 1.0), (1, 0.5), (2, 0.2)):
+        js = np.nonzero(rng.random(len(ksz)) < occ)[0]
+        bi.append(np.full(len(js), i, np.int64))
+        bj.append(js.astype(np.int64))
+    bi, bj = np.concatenate(bi), np.concatenate(bj)
+    order = np.lexsort((bj, bi))
+    bi, bj = bi[order], bj[order]
+    n = int(np.sum(rsz[bi].astype(np.int64) * ksz[bj]))
+    return Blocks(rsz, ksz, bi, bj, rng.standard_normal(n))
+
+
+@pytest.mark.parametrize("bands", [1, 3, 8])
+def test_column_bands(oracle, ctx, monkeypatch, bands):
+    """Work items segmented by column band (BT_BANDS): same C, any band count."""
+    monkeypatch.setenv("BT_BANDS", str(bands))
+    sz = np.array([13, 23], np.int32)[np.random.default_rng(3).integers(0, 2, 60)]
+    A, B, Cin = _case(oracle, 500 + bands, sz, sz, sz, 0.15, 0.15, 0.1)
+    want, nprod, _ = oracle.multiply(A, B, Cin)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    from paper_1910_13555_b200.store import multiply_local
+    st = multiply_local(ctx, a, b, c)
+    assert st["products"] == nprod
+    assert_parity(from_store(c), want)
+
+
+def test_export_to_pinned_and_pageable(oracle, ctx):
+    """bt_mat_export into page-locked and pageable host buffers (chunked
+    compaction + side-stream D2H) and put from a page-locked source."""
+    import torch
+    from oracle.oracle import Blocks
+    from paper_1910_13555_b200.store import LocalStore
+    sz = np.array([5, 13, 23, 8], np.int32)[np.random.default_rng(8).integers(0, 4, 50)]
+    A = oracle.random_matrix(801, sz, sz, 0.4)
+    src = torch.from_numpy(A.vals.copy()).pin_memory()
+    s = LocalStore(ctx, sz, sz)
+    s.put_blocks(A.bi, A.bj, src)
+    for pinned in (True, False):
+        out = torch.zeros(len(A.vals), dtype=torch.float64)
+        if pinned:
+            out = out.pin_memory()
+        bi, bj, v = s.export(out)
+        assert np.array_equal(bi, A.bi) and np.array_equal(bj, A.bj)
+        assert np.array_equal(v.numpy(), A.vals)
+    s.close()
