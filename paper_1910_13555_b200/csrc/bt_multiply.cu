@@ -37,16 +37,17 @@ constexpr int kMaxBands = 8;
 constexpr int NSEG = NCLASS * kMaxBands;
 constexpr uint32_t kCinFlag = 0x80000000u;
 
-// Tile classes: 16 DMMA tile shapes (ceil(m/8) in 1..4 -- taller blocks are cut
-// in 32-row tiles -- times ceil(n/8) in 1..4) + GENERIC (n > 32 or k > 64).
-__host__ __device__ inline int shape_class(int m, int n, bool dmma_ok) {
+// Tile classes: 16 DMMA tile shapes (ceil(m/8) in 1..4 -- blocks taller than
+// `tr` rows (24 or 32) are cut in tr-row tiles -- times ceil(n/8) in 1..4) +
+// GENERIC (n > 32 or k > 64).
+__host__ __device__ inline int shape_class(int m, int n, bool dmma_ok, int tr) {
   if (!dmma_ok || n > 32) return GENERIC;
-  const int mc = m > 32 ? 4 : (m + 7) / 8;
+  const int mc = m > tr ? tr / 8 : (m + 7) / 8;
   const int nc = (n + 7) / 8;
   return (mc - 1) * 4 + (nc - 1);
 }
-__host__ __device__ inline int class_tiles(int m, int cls) {
-  return (cls != GENERIC && m > 32) ? (m + 31) / 32 : 1;
+__host__ __device__ inline int class_tiles(int m, int cls, int tr) {
+  return (cls != GENERIC && m > tr) ? (m + tr - 1) / tr : 1;
 }
 
 __device__ __forceinline__ bool keep_product(const double* na, const double* nb, int32_t e,
@@ -67,6 +68,7 @@ struct RowArgs {
   int nbands;     // column bands of the numeric sweep (1..kMaxBands)
   int sort_min;   // rows with more A entries per chunk emit by window sort
   bool colmask;   // k_row_fill has a 64-bit per-column mask array (N <= kMaskCols)
+  int tall_rows;  // tile height for blocks taller than 32 rows (24 or 32)
   bool dmma_ok;
   // pass 1 outputs
   int32_t* row_nnz;
@@ -241,9 +243,10 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
     prods += v & ~kCinFlag;
     vals += t8_size(m, n);
     elems += static_cast<long long>(m) * n;
-    const int cls = shape_class(m, n, g.dmma_ok);
+    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
     const int seg = cls * kMaxBands + band_of(j, g);
-    agg_add(&cls_items[seg], seg, static_cast<unsigned long long>(class_tiles(m, cls)));
+    agg_add(&cls_items[seg], seg,
+            static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
   }
   using BR = cub::BlockReduce<long long, kChunkA>;
   __shared__ typename BR::TempStorage tmp;
@@ -324,9 +327,10 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         g.out_p0[c] = pbase + run_prod + p_ex;
         cur[j] = static_cast<int32_t>(run_prod + p_ex);
         cnt[j] = static_cast<uint32_t>(q);
-        const int cls = shape_class(m, n, g.dmma_ok);
+        const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
         const int seg = cls * kMaxBands + band_of(j, g);
-        agg_add(&cls_n[seg], seg, static_cast<unsigned long long>(class_tiles(m, cls)));
+        agg_add(&cls_n[seg], seg,
+                static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
       }
       run_prod += p_tot;
       run_val += v_tot;
@@ -347,20 +351,20 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   for (int32_t c = cbase + threadIdx.x; c < g.out_rp[i + 1]; c += blockDim.x) {
     const int j = g.out_col[c];
     const int n = g.n_sz[j];
-    const int cls = shape_class(m, n, g.dmma_ok);
-    const int nt = class_tiles(m, cls);
+    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
+    const int nt = class_tiles(m, cls, g.tall_rows);
     const int seg = cls * kMaxBands + band_of(j, g);
     const unsigned long long at = agg_add(&cls_at[seg], seg, static_cast<unsigned long long>(nt));
     const int64_t cin = g.cin_map[c];
     const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
     for (int q = 0; q < nt; ++q) {
-      const int r0 = 32 * q;
+      const int r0 = g.tall_rows * q;
       Item it;
       it.c_off = g.out_off[c] + (r0 >> 3) * tile_row;
       it.cin_off = cin >= 0 ? cin + (r0 >> 3) * tile_row : -1;
       it.p0r8 = g.out_p0[c] | (static_cast<int64_t>(r0 >> 3) << 48);
       it.np = g.out_np[c];
-      it.rows = static_cast<int16_t>(nt > 1 ? min(32, m - r0) : m);
+      it.rows = static_cast<int16_t>(nt > 1 ? min(g.tall_rows, m - r0) : m);
       it.n = static_cast<int16_t>(n);
       g.items[at + q] = it;
     }
@@ -759,6 +763,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.dmma_ok = dmma_ok;
     ra.sort_min = env_int("BT_SORT_MIN", 48);
     ra.colmask = colmask;
+    ra.tall_rows = env_int("BT_TALL_ROWS", 32) == 24 ? 24 : 32;
     {
       // column bands: when A and B together overflow a comfortable share of L2
       // (but are not in the K-panel regime below), sweep C in bands of B
