@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         bulk_g2s(st, g.at + (static_cast<int64_t>(d.x) + static_cast<int64_t>(p_r8) * KT) * 64,
                  ba, &bars[s]);
         bulk_g2s(st + g.a_region, g.bt + static_cast<int64_t>(d.y) * 64, bb, &bars[s]);
+        // (an L2 bulk prefetch of the following product measured 1-3 % slower)
       }
       ++issued;
       ++p_pos;
