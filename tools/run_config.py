@@ -37,7 +37,7 @@ def blocks_random(rng, rsz, csz, occ, scale_exp=0.0, band=None):
     return bi.astype(np.int64), bj.astype(np.int64), vals
 
 
-def config(name, rng):
+def config(name, rng, occ=None):
     """returns (rsz, ksz, nsz, A, B, eps, description)"""
     if name == "c2":
         sizes = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 1463)]
@@ -49,10 +49,11 @@ def config(name, rng):
     if name == "c3":
         m = np.full(100, 20, np.int32)
         k = np.full(20000, 20, np.int32)
-        A = blocks_random(rng, m, k, 0.10)
-        B = blocks_random(rng, k, m, 0.10)
+        o = 0.10 if occ is None else occ
+        A = blocks_random(rng, m, k, o)
+        B = blocks_random(rng, k, m, o)
         return m, k, m, A, B, 0.0, ("c3: C 2000x2000 = A 2000x400000 * B 400000x2000, "
-                                    "blocks 20, occ 0.10 (single GPU, local multiply)")
+                                    f"blocks 20, occ {o:.2f} (single GPU, local multiply)")
     if name == "c4":
         ao = np.tile(np.array([13, 23], np.int32), 100)       # a, b: 200 AO blocks
         aux = np.tile(np.array([13, 23], np.int32), 200)      # P, Q: 400 aux blocks
@@ -70,12 +71,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--cpu", action="store_true", help="also time the reference on 1 core")
+    ap.add_argument("--occ", type=float, default=None, help="c3: block occupancy (0.10-0.50)")
     args = ap.parse_args()
     import torch
     from paper_1910_13555_b200.store import Context, LocalStore, multiply_local
     rng = np.random.default_rng(2024)
     t0 = time.time()
-    rsz, ksz, nsz, A, B, eps, desc = config(args.config, rng)
+    rsz, ksz, nsz, A, B, eps, desc = config(args.config, rng, args.occ)
     gen_s = time.time() - t0
     ctx = Context(0)
     ctx.set_timing(True)
