@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -273,6 +274,9 @@ struct Grid {
   DBuf<int64_t> gather_sizes;
   DBuf<int32_t> gather_idx;    // P packed index segments (allgather path)
   cudaEvent_t phase_ev = nullptr;  // BT_PHASES: recorded at the numeric start
+  cudaEvent_t ev_sizes = nullptr;  // size round of the gather read back
+  int64_t spec_capb = 0, spec_capv = 0;  // speculative segment capacities
+  bool spec_last = false;
   DBuf<int32_t> gather_rdist;  // row -> owning rank of the gathered slabs
   std::vector<int32_t> gather_rdist_h;
   bool is_local(int r) const { return r >= first && r < first + nlocal; }
@@ -604,9 +608,10 @@ void add_stats(bt_stats& acc, const bt_stats& s) {
 }
 
 void rank_multiply(Ctx* ctx, const Mat& a, const Mat& b, Mat& c, double eps, bt_stats& acc,
-                   cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr) {
+                   cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr,
+                   const std::function<void()>* after_sizes = nullptr) {
   bt_stats s{};
-  local_multiply(*ctx, a, b, c, eps, &s, wait_numeric, numeric_start);
+  local_multiply(*ctx, a, b, c, eps, &s, wait_numeric, numeric_start, after_sizes);
   add_stats(acc, s);
 }
 
@@ -834,17 +839,22 @@ cudaEvent_t gather_rows_nccl(Grid& g, const Mat& mine, const std::vector<int32_t
 // per block row.
 __global__ void k_assemble_gathered(const int32_t* __restrict__ gidx, int64_t seg, int64_t colb,
                                     int64_t offb, int P, const int32_t* __restrict__ rdist,
-                                    int64_t nbr, int64_t maxv, int32_t* __restrict__ rp,
-                                    int32_t* __restrict__ col, int64_t* __restrict__ off) {
+                                    int64_t nbr, int64_t maxv, int64_t capb,
+                                    int32_t* __restrict__ rp, int32_t* __restrict__ col,
+                                    int64_t* __restrict__ off) {
   const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i > nbr) return;
+  // a slab larger than the segment capacity (a missed speculation, redone by
+  // the host) is treated as empty so every read stays inside the buffers
   int32_t dst = 0;
-  for (int q = 0; q < P; ++q) dst += gidx[q * seg + i];
+  for (int q = 0; q < P; ++q)
+    if (gidx[q * seg + nbr] <= capb) dst += gidx[q * seg + i];
   if (lane == 0) rp[i] = dst;
   if (i == nbr) return;
   const int p = rdist[i];
   const int32_t* s = gidx + p * seg;
+  if (s[nbr] > capb) return;
   const int32_t e0 = s[i], n = s[i + 1] - e0;
   const int32_t* sc = s + colb;
   const int64_t* so = reinterpret_cast<const int64_t*>(s + offb);
@@ -855,15 +865,56 @@ __global__ void k_assemble_gathered(const int32_t* __restrict__ gidx, int64_t se
   }
 }
 
-// All-gather of row slabs into one store with two in-place ncclAllGather calls
-// (every rank of the communicator takes part): the packed index (row_ptr | col
-// | off, padded to the largest slab) and the T8 values (padded likewise).  One
-// size round first (the counts NCCL needs), then both gathers are enqueued on
-// the comm stream at once; the index is assembled by one kernel on the main
-// stream as soon as it lands, while the values keep streaming.  Returns the
-// event recorded when the values have landed.
+// All-gather of row slabs into one store with in-place ncclAllGather calls
+// (every rank of the communicator takes part): a 3-word size round, the packed
+// index (row_ptr | col | off, one segment per rank) and the T8 values (one
+// segment per rank), all on the comm stream; the index is assembled by one
+// kernel on the main stream as soon as it lands while the values keep
+// streaming.  Returns the event recorded when the values have landed.
+//
+// Segment capacities.  exact (spec = false): the host waits for the size
+// round and sizes the segments to the largest slab.  spec = true: the
+// segments take the capacities remembered from earlier calls and there is no
+// size round (the sizes ride in the index segments' headers), so the index
+// and value rounds are enqueued at once without any host wait;
+// gather_check() (run by the multiply right after its own pass-1 sync, before
+// any value is read) confirms every slab fit, or throws SpecMiss and the caller
+// redoes the gather exactly.  All ranks see the same sizes, so they all take
+// the same branch.
+struct SpecMiss {};
+
+// Sizes of the last gather: exact store metadata and ledger charges; in the
+// speculative case throws SpecMiss when a slab did not fit its segment.
+void gather_check(Grid& g, const Mat& mine, int nprocs, Mat& full, bool spec) {
+  Ctx& x = *g.ctx;
+  BT_CUDA(cudaEventSynchronize(g.ev_sizes));
+  const int64_t* h = reinterpret_cast<const int64_t*>(x.pinned) + 384;
+  int64_t nblk = 0, nel = 0, maxb = 0, maxv = 0;
+  for (int p = 0; p < nprocs; ++p) {
+    nblk += h[8 + 3 * p];
+    maxb = std::max(maxb, h[8 + 3 * p]);
+    maxv = std::max(maxv, h[8 + 3 * p + 1]);
+    nel += h[8 + 3 * p + 2];
+  }
+  if (spec && (maxb > g.spec_capb || maxv > g.spec_capv)) throw SpecMiss{};
+  // next call's capacities: 1/8 headroom over this call, decaying slowly
+  // when the slabs shrink (identical on every rank: same sizes)
+  g.spec_capb = std::max(maxb + maxb / 8, g.spec_capb - g.spec_capb / 8);
+  g.spec_capv = std::max((maxv + maxv / 8 + 63) & ~int64_t(63),
+                         (g.spec_capv - g.spec_capv / 8 + 63) & ~int64_t(63));
+  if (env_int("BT_GATHER_SPEC_TEST", 0)) {  // tests: force the next speculation to miss
+    g.spec_capb = maxb / 2;
+    g.spec_capv = (maxv / 2) & ~int64_t(63);
+  }
+  full.nblk = nblk;
+  full.nelems = nel;
+  const int me = g.first;
+  g.charge_send(me, (nprocs - 1) * mine.nelems, (nprocs - 1) * 4 * mine.nblk);
+  g.charge_recv(me, nel - mine.nelems, 4 * (nblk - mine.nblk));
+}
+
 cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<int32_t>& rdist,
-                                  int nprocs, Mat& full) {
+                                  int nprocs, Mat& full, bool spec) {
   Ctx& x = *g.ctx;
   Trace tr("gather");
   ncclComm_t comm = static_cast<ncclComm_t>(x.nccl);
@@ -879,14 +930,16 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
     BT_CUDA(cudaEventSynchronize(pev[5]));
     float t[5];
     for (int q = 0; q < 5; ++q) BT_CUDA(cudaEventElapsedTime(&t[q], pev[0], pev[q + 1]));
-    fprintf(stderr, "[bt-gather] sizes %.1f | index %.1f | assembled %.1f | values %.1f | "
-                    "numeric start %.1f us\n", 1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3],
-            1e3 * t[4]);
+    fprintf(stderr, "[bt-gather] %s sizes %.1f | index %.1f | assembled %.1f | values %.1f | "
+                    "numeric start %.1f us\n", g.spec_last ? "spec" : "exact", 1e3 * t[0],
+            1e3 * t[1], 1e3 * t[2], 1e3 * t[3], 1e3 * t[4]);
   }
+  g.spec_last = spec;
   auto grow = [&](auto& buf, size_t n) {
     if (buf.n < n) buf.alloc(n + n / 8, x.stream);
   };
-  int64_t* h = reinterpret_cast<int64_t*>(x.pinned) + 64;
+  // pinned words [384, 384 + 8 + 3P): clear of the multiply's size readback
+  int64_t* h = reinterpret_cast<int64_t*>(x.pinned) + 384;
   h[0] = mine.nblk;
   h[1] = mine.nvals;
   h[2] = mine.nelems;
@@ -898,37 +951,32 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
                             cudaMemcpyHostToDevice, x.stream));
   }
   const int64_t nbr = full.nbr;
-  // Index segment capacity.  Default: a size round fixes the exact maximum
-  // first.  BT_GATHER_ONE_ROUND=1: every rank bounds a slab's block count by
-  // its rows x all columns without communication and the index goes out at
-  // once with a 3-word size header in front -- measured slower on 4 B200s
-  // (the padded index round and the later host sync cost more than the size
-  // round saves), kept as an option.
-  std::vector<int64_t> rows_of(nprocs, 0);
-  for (int32_t p : rdist)
-    if (p >= 0 && p < nprocs) ++rows_of[p];
-  const int64_t cap = *std::max_element(rows_of.begin(), rows_of.end()) * full.nbc;
-  const bool one_round = cap * 12 <= (int64_t(64) << 20) && env_int("BT_GATHER_ONE_ROUND", 0) == 1;
-  ncclResult_t r;
-  int64_t maxb;
   BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
   if (phases) BT_CUDA(cudaEventRecord(pev[0], x.stream));
   BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
-  if (one_round) {
-    maxb = cap;
+  ncclResult_t r;
+  int64_t maxb, maxv;
+  if (spec) {
+    // no size round: the sizes travel in the index segments' headers
+    maxb = g.spec_capb;
+    maxv = g.spec_capv;
     if (phases) BT_CUDA(cudaEventRecord(pev[1], cs));
   } else {
     grow(g.gather_sizes, static_cast<size_t>(3 * nprocs));
     DBuf<int64_t>& dsz = g.gather_sizes;
     BT_CUDA(cudaMemcpyAsync(dsz.p + 3 * me, h, 24, cudaMemcpyHostToDevice, cs));
     r = ncclAllGather(dsz.p + 3 * me, dsz.p, 3, ncclInt64, comm, cs);
-    if (phases) BT_CUDA(cudaEventRecord(pev[1], cs));
     BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL,
                std::string("NCCL size gather: ") + ncclGetErrorString(r));
     BT_CUDA(cudaMemcpyAsync(h + 8, dsz.p, 24 * nprocs, cudaMemcpyDeviceToHost, cs));
-    BT_CUDA(cudaStreamSynchronize(cs));
-    maxb = 0;
-    for (int p = 0; p < nprocs; ++p) maxb = std::max(maxb, h[8 + 3 * p]);
+    BT_CUDA(cudaEventRecord(g.ev_sizes, cs));
+    if (phases) BT_CUDA(cudaEventRecord(pev[1], cs));
+    BT_CUDA(cudaEventSynchronize(g.ev_sizes));
+    maxb = maxv = 0;
+    for (int p = 0; p < nprocs; ++p) {
+      maxb = std::max(maxb, h[8 + 3 * p]);
+      maxv = std::max(maxv, h[8 + 3 * p + 1]);
+    }
   }
   tr.mark("sizes");
   // segment (int32 words): header (3 x int64) | row_ptr | col | off
@@ -937,41 +985,31 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
   const int64_t offb = colb + pad2(maxb);
   const int64_t seg = offb + 2 * maxb;
   grow(g.gather_idx, static_cast<size_t>(seg * nprocs));
+  grow(full.row_ptr, static_cast<size_t>(nbr + 1));
+  grow(full.col, static_cast<size_t>(std::max<int64_t>(maxb * nprocs, 1)));
+  grow(full.off, static_cast<size_t>(std::max<int64_t>(maxb * nprocs, 1)));
+  grow(full.vals, static_cast<size_t>(std::max<int64_t>(maxv * nprocs, 64)));
+  full.nblk = maxb * nprocs;  // upper bound until the sizes are known (gather_check)
+  full.nvals = maxv * nprocs;
+  full.nelems = 0;
+  BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
+  BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
+  // my slab into my segments (clamped: a slab over capacity is a miss anyway)
+  const int64_t sb = std::min(mine.nblk, maxb), sv = std::min(mine.nvals, maxv);
   int32_t* mseg = g.gather_idx.p + seg * me;
   BT_CUDA(cudaMemcpyAsync(mseg, h, 24, cudaMemcpyHostToDevice, cs));
   BT_CUDA(cudaMemcpyAsync(mseg + rpb, mine.row_ptr.p, 4 * (nbr + 1), cudaMemcpyDeviceToDevice, cs));
-  if (mine.nblk) {
-    BT_CUDA(cudaMemcpyAsync(mseg + colb, mine.col.p, 4 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
-    BT_CUDA(cudaMemcpyAsync(mseg + offb, mine.off.p, 8 * mine.nblk, cudaMemcpyDeviceToDevice, cs));
+  if (sb) {
+    BT_CUDA(cudaMemcpyAsync(mseg + colb, mine.col.p, 4 * sb, cudaMemcpyDeviceToDevice, cs));
+    BT_CUDA(cudaMemcpyAsync(mseg + offb, mine.off.p, 8 * sb, cudaMemcpyDeviceToDevice, cs));
   }
   r = ncclAllGather(mseg, g.gather_idx.p, seg, ncclInt32, comm, cs);
   BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL index gather: ") + ncclGetErrorString(r));
   BT_CUDA(cudaEventRecord(g.ev_idx, cs));
-  if (one_round) {  // the headers: one strided readback
-    BT_CUDA(cudaMemcpy2DAsync(h + 8, 24, g.gather_idx.p, 4 * seg, 24, nprocs,
-                              cudaMemcpyDeviceToHost, cs));
-    BT_CUDA(cudaStreamSynchronize(cs));
-  }
-  tr.mark("index");
-  int64_t nblk = 0, maxv = 0, nel = 0;
-  for (int p = 0; p < nprocs; ++p) {
-    nblk += h[8 + 3 * p];
-    maxv = std::max(maxv, h[8 + 3 * p + 1]);
-    nel += h[8 + 3 * p + 2];
-  }
-  grow(full.row_ptr, static_cast<size_t>(nbr + 1));
-  grow(full.col, static_cast<size_t>(std::max<int64_t>(nblk, 1)));
-  grow(full.off, static_cast<size_t>(std::max<int64_t>(nblk, 1)));
-  grow(full.vals, static_cast<size_t>(std::max<int64_t>(maxv * nprocs, 64)));
-  full.nblk = nblk;
-  full.nvals = maxv * nprocs;
-  full.nelems = nel;
-  BT_CUDA(cudaEventRecord(g.ev_main, x.stream));
-  BT_CUDA(cudaStreamWaitEvent(cs, g.ev_main, 0));
   if (phases) BT_CUDA(cudaEventRecord(pev[2], cs));
   if (maxv) {
-    if (mine.nvals)
-      BT_CUDA(cudaMemcpyAsync(full.vals.p + maxv * me, mine.vals.p, 8 * mine.nvals,
+    if (sv)
+      BT_CUDA(cudaMemcpyAsync(full.vals.p + maxv * me, mine.vals.p, 8 * sv,
                               cudaMemcpyDeviceToDevice, cs));
     r = ncclAllGather(full.vals.p + maxv * me, full.vals.p, maxv, ncclFloat64, comm, cs);
     BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL,
@@ -981,8 +1019,13 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
   if (phases) BT_CUDA(cudaEventRecord(pev[4], cs));
   tr.mark("enqueue rounds");
   BT_CUDA(cudaStreamWaitEvent(x.stream, g.ev_idx, 0));
+  if (spec) {  // the headers of the landed index segments, for gather_check
+    BT_CUDA(cudaMemcpy2DAsync(h + 8, 24, g.gather_idx.p, 4 * seg, 24, nprocs,
+                              cudaMemcpyDeviceToHost, x.stream));
+    BT_CUDA(cudaEventRecord(g.ev_sizes, x.stream));
+  }
   k_assemble_gathered<<<nb((nbr + 1) * 32, 256), 256, 0, x.stream>>>(
-      g.gather_idx.p + rpb, seg, colb - rpb, offb - rpb, nprocs, g.gather_rdist.p, nbr, maxv,
+      g.gather_idx.p + rpb, seg, colb - rpb, offb - rpb, nprocs, g.gather_rdist.p, nbr, maxv, maxb,
       full.row_ptr.p, full.col.p, full.off.p);
   check_launch("assemble_gathered");
   count_launch(&x);
@@ -992,8 +1035,7 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
     pev_recorded = true;
   }
   tr.mark("assemble");
-  g.charge_send(me, (nprocs - 1) * mine.nelems, (nprocs - 1) * 4 * mine.nblk);
-  g.charge_recv(me, nel - mine.nelems, 4 * (nblk - mine.nblk));
+  if (!spec) gather_check(g, mine, nprocs, full, false);
   return g.ev_comm;
 }
 
@@ -1136,12 +1178,27 @@ void case2(const DMat& a, const DMat& b, DMat& c, int nprocs, int gather, double
     if (!g.gather_full || g.gather_full->impl.h_rsz != b.rsz || g.gather_full->impl.h_csz != b.csz)
       g.gather_full = new_store(g.ctx, b.rsz, b.csz);
     Mat& full = g.gather_full->impl;
-    // every rank of the communicator in the gather: two collective calls;
+    // every rank of the communicator in the gather: collective calls (with
+    // speculative segment capacities once a first call has sized them, eps = 0);
     // a sub-group: point-to-point rounds
-    cudaEvent_t vals_ready = nprocs == g.P && env_int("BT_GATHER_P2P", 0) == 0
-                                 ? gather_rows_allgather(g, bl.view->store(r), ks, nprocs, full)
-                                 : gather_rows_nccl(g, bl.view->store(r), ks, nprocs, full);
-    rank_multiply(g.ctx, al.view->store(r), full, cl->store(r), eps, S, vals_ready, g.phase_ev);
+    if (nprocs == g.P && env_int("BT_GATHER_P2P", 0) == 0) {
+      bool spec = eps == 0.0 && g.spec_capb > 0 && env_int("BT_GATHER_SPEC", 1) != 0;
+      const Mat& mine = bl.view->store(r);
+      for (;;) {
+        cudaEvent_t vals_ready = gather_rows_allgather(g, mine, ks, nprocs, full, spec);
+        try {
+          std::function<void()> check = [&] { gather_check(g, mine, nprocs, full, true); };
+          rank_multiply(g.ctx, al.view->store(r), full, cl->store(r), eps, S, vals_ready,
+                        g.phase_ev, spec ? &check : nullptr);
+          break;
+        } catch (const SpecMiss&) {
+          spec = false;  // a slab outgrew its segment: redo exactly (capacities grow)
+        }
+      }
+    } else {
+      cudaEvent_t vals_ready = gather_rows_nccl(g, bl.view->store(r), ks, nprocs, full);
+      rank_multiply(g.ctx, al.view->store(r), full, cl->store(r), eps, S, vals_ready, g.phase_ev);
+    }
     g.phase_ev = nullptr;
   } else if (gather) {
     // all-gather of the B slabs
@@ -1242,6 +1299,7 @@ int bt_grid_create(bt_ctx* ctx, int nranks, bt_grid** out) {
     BT_CUDA(cudaEventCreateWithFlags(&G.ev_comm, cudaEventDisableTiming));
     BT_CUDA(cudaEventCreateWithFlags(&G.ev_main, cudaEventDisableTiming));
     BT_CUDA(cudaEventCreateWithFlags(&G.ev_idx, cudaEventDisableTiming));
+    BT_CUDA(cudaEventCreateWithFlags(&G.ev_sizes, cudaEventDisableTiming));
     G.totals.assign(nranks, Counters{});
     G.phases.assign(nranks, {});
     G.phase.assign(nranks, "");
@@ -1261,6 +1319,7 @@ int bt_grid_destroy(bt_grid* g) {
     if (G.ev_comm) cudaEventDestroy(G.ev_comm);
     if (G.ev_main) cudaEventDestroy(G.ev_main);
     if (G.ev_idx) cudaEventDestroy(G.ev_idx);
+    if (G.ev_sizes) cudaEventDestroy(G.ev_sizes);
     delete g;
   });
 }

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "btcuda.h"
@@ -209,7 +210,8 @@ void upload_parts(Ctx& x, const HostPart* parts, int n, void* const* dst);
 // wait_numeric (optional): the numeric phase waits for this event (B's values
 // may still be in flight while the symbolic passes run).
 void local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& C, double eps, bt_stats* stats,
-                    cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr);
+                    cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr,
+                    const std::function<void()>* after_sizes = nullptr);
 
 }  // namespace bt
 

@@ -699,7 +699,8 @@ using namespace bt;
 
 // The local multiply C += A*B (one rank's stores); throws bt::Error.
 void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps, bt_stats* stats,
-                        cudaEvent_t wait_numeric, cudaEvent_t numeric_start) {
+                        cudaEvent_t wait_numeric, cudaEvent_t numeric_start,
+                        const std::function<void()>* after_sizes) {
   {
     BT_REQUIRE(A.ctx == &x && B.ctx == &x && Cm.ctx == &x, BT_ERR_INVALID_ARGUMENT,
                "bt_multiply: matrices belong to another context");
@@ -836,6 +837,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     tr.mark("pass1 enqueued");
     BT_CUDA(cudaStreamSynchronize(st));
     tr.mark("pass1 sync");
+    // caller's check between the sizes and any use of B's values (the
+    // speculative case-2 gather confirms its segments here, or throws)
+    if (after_sizes) (*after_sizes)();
     const int64_t nout = static_cast<int64_t>(h.nout), nprod = static_cast<int64_t>(h.nprod),
                   nvals = static_cast<int64_t>(h.nvals);
     S.candidates = static_cast<int64_t>(h.tot[0]);

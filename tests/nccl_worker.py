@@ -79,13 +79,20 @@ def main():
     if q * q == world:
         cases.append(("cannon", q))
     cases += [("case1", 1), ("case2", 1), ("case2g", 1)]
+    # the B gather again on the same communicator: speculative segment
+    # capacities (a slightly smaller B fits; a much denser one misses and is
+    # redone exactly), then eps > 0 (always exact)
+    cases += [("case2g-spec", 1, 21, 0.40), ("case2g-miss", 1, 31, 0.85),
+              ("case2g-spec2", 1, 41, 0.80)]
     rs = np.array([5, 13, 23, 7, 13, 5, 23, 11, 9, 17, 4, 23], np.int32)
     ks = np.array([13, 5, 23, 8, 16, 23, 5, 13], np.int32)
     ns = np.array([23, 7, 5, 13, 20, 9, 23], np.int32)
-    for algo, gq in cases:
-        A = o.random_matrix(11, rs, ks, 0.45)
-        B = o.random_matrix(12, ks, ns, 0.45)
-        Cin = o.random_matrix(13, rs, ns, 0.2)
+    for case in cases:
+        algo, gq = case[0], case[1]
+        seed, occ = (case[2], case[3]) if len(case) > 2 else (11, 0.45)
+        A = o.random_matrix(seed, rs, ks, occ)
+        B = o.random_matrix(seed + 1, ks, ns, occ)
+        Cin = o.random_matrix(seed + 2, rs, ns, 0.2)
         grid = d.ProcessGrid([gq, gq])
         a, b, c = build(A, grid, comm), build(B, grid, comm), build(Cin, grid, comm)
         if algo == "cannon":
@@ -93,7 +100,7 @@ def main():
         elif algo == "case1":
             st = d.multiply_reduce_case1(comm, a, b, c, world)
         else:
-            st = d.multiply_virtual_case2(comm, a, b, c, world, gather=(algo == "case2g"))
+            st = d.multiply_virtual_case2(comm, a, b, c, world, gather=algo.startswith("case2g"))
         got = gather_c(c)
         if rank == 0:
             want, _, _ = o.multiply(A, B, Cin)
