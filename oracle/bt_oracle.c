@@ -191,9 +191,16 @@ void bto_block_gemm_acc(double* c, const double* a, const double* b, int m, int 
     }
 }
 
-double bto_block_norm(const double* a, int64_t n) {
+/* Block Frobenius norm (the build-defined eps filter): squares
+   summed along each row first, then the row sums in row order; unfused
+   (-ffp-contract=off).  The GPU (k_block_norms) adds in the same order. */
+double bto_block_norm(const double* a, int m, int n) {
   double s = 0.0;
-  for (int64_t t = 0; t < n; ++t) s += a[t] * a[t];
+  for (int r = 0; r < m; ++r) {
+    double rs = 0.0;
+    for (int c = 0; c < n; ++c) rs += a[(size_t)r * n + c] * a[(size_t)r * n + c];
+    s += rs;
+  }
   return sqrt(s);
 }
 
@@ -230,10 +237,10 @@ int bto_multiply(const bto_mat* a, const bto_mat* b, bto_mat* c, double eps, int
     nb = (double*)malloc(sizeof(double) * (size_t)(b->nblk + 1));
     for (int64_t r = 0; r < a->nbr; ++r)
       for (int64_t e = a->row_ptr[r]; e < a->row_ptr[r + 1]; ++e)
-        na[e] = bto_block_norm(a->vals + a->off[e], (int64_t)a->rsz[r] * a->csz[a->col[e]]);
+        na[e] = bto_block_norm(a->vals + a->off[e], a->rsz[r], a->csz[a->col[e]]);
     for (int64_t r = 0; r < b->nbr; ++r)
       for (int64_t e = b->row_ptr[r]; e < b->row_ptr[r + 1]; ++e)
-        nb[e] = bto_block_norm(b->vals + b->off[e], (int64_t)b->rsz[r] * b->csz[b->col[e]]);
+        nb[e] = bto_block_norm(b->vals + b->off[e], b->rsz[r], b->csz[b->col[e]]);
   }
 
   bto_mat out;
@@ -328,7 +335,7 @@ int bto_filter(bto_mat* c, double eps) {
     int64_t start = nb;
     for (int64_t e = c->row_ptr[i]; e < c->row_ptr[i + 1]; ++e) {
       int64_t sz = (int64_t)c->rsz[i] * c->csz[c->col[e]];
-      double nrm = bto_block_norm(c->vals + c->off[e], sz);
+      double nrm = bto_block_norm(c->vals + c->off[e], c->rsz[i], c->csz[c->col[e]]);
       if (nrm < eps) continue;
       memmove(c->vals + nv, c->vals + c->off[e], sizeof(double) * (size_t)sz);
       c->col[nb] = c->col[e];

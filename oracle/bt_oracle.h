@@ -79,7 +79,7 @@ int64_t bto_random_blocking(uint64_t seed, int64_t total, int bmin, int bmax, in
 void bto_block_gemm_acc(double* c, const double* a, const double* b, int m, int n, int k);
 
 /* Frobenius norm of a block: sequential sum of squares (no FMA), sqrt. */
-double bto_block_norm(const double* a, int64_t n);
+double bto_block_norm(const double* a, int m, int n);
 
 /* Local multiply C += A*B with reference semantics: multiply_tiles_into
  * (multiply_cannon.hpp:24-44) + order_batches (block.hpp:112-118) +

@@ -187,7 +187,8 @@ struct Trace {
 // launch accounting
 inline void count_launch(Ctx* c, int n = 1) { c->kernels += n; }
 
-// implemented in bt_store.cu
+// implemented in bt_store.cu (one warp per block)
+constexpr int kNormThreads = 256;
 __global__ void k_block_norms(const double* vals, const int32_t* row_ptr, const int32_t* col,
                               const int64_t* off, const int32_t* rsz, const int32_t* csz,
                               int64_t nbr, double* out, int64_t nblk);

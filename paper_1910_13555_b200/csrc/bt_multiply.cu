@@ -732,12 +732,10 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     if (eps > 0 && A.nblk && B.nblk) {
       na.alloc(A.nblk, st);
       nb.alloc(B.nblk, st);
-      k_block_norms<<<blocks_for(A.nblk, 128), 128, 0, st>>>(A.vals.p, A.row_ptr.p, A.col.p,
-                                                              A.off.p, A.rsz.p, A.csz.p, A.nbr,
-                                                              na.p, A.nblk);
-      k_block_norms<<<blocks_for(B.nblk, 128), 128, 0, st>>>(B.vals.p, B.row_ptr.p, B.col.p,
-                                                              B.off.p, B.rsz.p, B.csz.p, B.nbr,
-                                                              nb.p, B.nblk);
+      k_block_norms<<<blocks_for(A.nblk * 32, kNormThreads), kNormThreads, 0, st>>>(
+          A.vals.p, A.row_ptr.p, A.col.p, A.off.p, A.rsz.p, A.csz.p, A.nbr, na.p, A.nblk);
+      k_block_norms<<<blocks_for(B.nblk * 32, kNormThreads), kNormThreads, 0, st>>>(
+          B.vals.p, B.row_ptr.p, B.col.p, B.off.p, B.rsz.p, B.csz.p, B.nbr, nb.p, B.nblk);
       check_launch("block_norms");
       count_launch(&x, 2);
     }

@@ -224,12 +224,17 @@ __global__ void k_compact(double* __restrict__ dst, const int64_t* __restrict__ 
   }
 }
 
-// Frobenius norm per block: sequential sum of squares, unfused.
+// Frobenius norm per block: squares summed along each row, then
+// the row sums added in row order; unfused, so the oracle's identical loop
+// gives identical bits.  One warp per block, one lane per row (32 rows at a
+// time): the dependent chain is n + m additions, not m * n.
+// Launch with kNormThreads threads per CTA.
 __global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __restrict__ row_ptr,
                               const int32_t* __restrict__ col, const int64_t* __restrict__ off,
                               const int32_t* __restrict__ rsz, const int32_t* __restrict__ csz,
                               int64_t nbr, double* __restrict__ out, int64_t nblk) {
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (b >= nblk) return;
   // row of entry b: binary search in row_ptr
   int64_t lo = 0, hi = nbr;
@@ -240,12 +245,35 @@ __global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __
   const int m = rsz[lo], n = csz[col[b]], ntc = tiles8(n);
   const double* p = vals + off[b];
   double s = 0.0;
-  for (int r = 0; r < m; ++r)  // row-major element order, as the reference stores it
-    for (int c = 0; c < n; ++c) {
-      const double v = p[t8_pos(r, c, ntc)];
-      s = __dadd_rn(s, __dmul_rn(v, v));
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    const int r = r0 + lane;
+    double rs = 0.0;
+    if (r < m) {
+      // row r, 8 columns per T8 tile: one contiguous 64-byte tile row, stored
+      // with the swizzle (column u at u ^ sw); the zero padding past column n
+      // adds +0.0, which leaves the (non-negative) sum bit-identical
+      const int sw = ((r >> 1) & 1) << 2;
+      const double2* tr = reinterpret_cast<const double2*>(p + (((r >> 3) * ntc) << 6) +
+                                                           ((r & 7) << 3));
+      for (int tc = 0; tc < ntc; ++tc) {
+        double w[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const double2 d = tr[(tc << 5) + h];  // tile tc: 64 doubles = 32 double2
+          w[2 * h] = d.x;
+          w[2 * h + 1] = d.y;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double v = sw ? w[u ^ 4] : w[u];
+          rs = __dadd_rn(rs, __dmul_rn(v, v));
+        }
+      }
     }
-  out[b] = __dsqrt_rn(s);
+    const int cnt = min(32, m - r0);
+    for (int k = 0; k < cnt; ++k) s = __dadd_rn(s, __shfl_sync(0xffffffffu, rs, k));
+  }
+  if (lane == 0) out[b] = __dsqrt_rn(s);
 }
 
 // ------------------------------------------------------------- host helpers
@@ -790,7 +818,8 @@ int bt_mat_norms(const bt_mat* mh, double* out) {
     if (m.nblk == 0) return;
     cudaStream_t st = m.stream();
     DBuf<double> d(m.nblk, st);
-    k_block_norms<<<static_cast<unsigned>((m.nblk + 127) / 128), 128, 0, st>>>(
+    k_block_norms<<<static_cast<unsigned>((m.nblk * 32 + kNormThreads - 1) / kNormThreads),
+                    kNormThreads, 0, st>>>(
         m.vals.p, m.row_ptr.p, m.col.p, m.off.p, m.rsz.p, m.csz.p, m.nbr, d.p, m.nblk);
     check_launch("block_norms");
     count_launch(m.ctx);
@@ -807,7 +836,8 @@ int bt_filter(bt_mat* mh, double eps) {
     cudaStream_t st = m.stream();
     std::vector<double> nrm(m.nblk);
     DBuf<double> d(m.nblk, st);
-    k_block_norms<<<static_cast<unsigned>((m.nblk + 127) / 128), 128, 0, st>>>(
+    k_block_norms<<<static_cast<unsigned>((m.nblk * 32 + kNormThreads - 1) / kNormThreads),
+                    kNormThreads, 0, st>>>(
         m.vals.p, m.row_ptr.p, m.col.p, m.off.p, m.rsz.p, m.csz.p, m.nbr, d.p, m.nblk);
     check_launch("block_norms");
     count_launch(m.ctx);
