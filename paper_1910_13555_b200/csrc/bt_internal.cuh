@@ -112,10 +112,10 @@ struct Ctx {
   cudaEvent_t stage_ev = nullptr;
   unsigned char* host_stage(size_t bytes);
   bool timing = false;          // record CUDA events around multiply kernels
-  static constexpr int kAux = 4;  // side streams: concurrent per-class numeric kernels
-  cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  static constexpr int kAux = 16;  // side streams: concurrent per-class numeric kernels
+  cudaStream_t aux[kAux] = {};
   cudaEvent_t ev_fork = nullptr;
-  cudaEvent_t ev_join[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_join[kAux] = {};
   cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   void* ensure_scratch(size_t bytes);
   // Grow-only per-slot workspace for call-local temporaries (no allocator calls
