@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -566,6 +567,48 @@ inline Algorithm select_algorithm(double m, double n, double k, double oa, doubl
     v = case1_volume(s);
   }
   if (case2_volume(s) < v) best = Algorithm::case2;
+  return best;
+}
+// Extension: NVLink/NVSwitch-aware time model, seconds per
+// multiply on s.nprocs B200s (mirror of dist.py predicted_time_b200).  Cannon
+// overlaps its shifts with the local multiply (square grids only); case 1's C
+// reduction follows the multiply; case 2's B gather is half hidden behind the
+// symbolic passes.
+struct B200Machine {
+  double fp64_flops = 26e12;  // k_smm_dmma useful FP64, c1
+  double link_bytes = 770e9;  // NVLink peer copy per direction
+  double hbm_bytes = 6.55e12; // HBM copy
+};
+inline double predicted_time_b200(Algorithm algo, const MultiplySpec& s,
+                                  const B200Machine& hw = B200Machine{}) {
+  s.validate();
+  const double p = s.nprocs;
+  const double flops = 2.0 * s.m * s.n * s.k * s.occ_a * s.occ_b;
+  const double compute = flops / (p * hw.fp64_flops) + 8.0 * s.stored_c() / p / hw.hbm_bytes;
+  switch (algo) {
+    case Algorithm::cannon: {
+      const double q = std::round(std::sqrt(p));
+      if (q * q != p) return std::numeric_limits<double>::infinity();
+      return std::max(compute, 8.0 * cannon_volume(s) / hw.link_bytes);
+    }
+    case Algorithm::case1: return compute + 8.0 * case1_volume(s) / hw.link_bytes;
+    case Algorithm::case2: return compute + 0.5 * 8.0 * case2_volume(s) / hw.link_bytes;
+  }
+  throw invalid_argument("predicted_time_b200: unknown algorithm");
+}
+inline Algorithm select_algorithm_b200(double m, double n, double k, double oa, double ob,
+                                       double oc, double p,
+                                       const B200Machine& hw = B200Machine{}) {
+  MultiplySpec s{m, n, k, oa, ob, oc, p};
+  Algorithm best = Algorithm::cannon;
+  double t = predicted_time_b200(best, s, hw);
+  for (Algorithm a : {Algorithm::case1, Algorithm::case2}) {
+    const double ta = predicted_time_b200(a, s, hw);
+    if (ta < t) {
+      best = a;
+      t = ta;
+    }
+  }
   return best;
 }
 inline MultiplySpec measured_spec(const DistMatrix& a, const DistMatrix& b, double occ_c,

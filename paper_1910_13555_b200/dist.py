@@ -587,6 +587,58 @@ def select_algorithm(m, n, k, occ_a, occ_b, occ_c_estimate, nprocs):
     return best
 
 
+@dataclass
+class B200Machine:
+    """Per-GPU rates of the time model (measured on this pool, profiles/):
+    useful FP64 of the local multiply, NVLink per direction, HBM copy."""
+    fp64_flops: float = 26e12     # k_smm_dmma, c1 (r01b)
+    link_bytes: float = 770e9     # peer copy, B200_PROFILING.md
+    hbm_bytes: float = 6.55e12    # MEASURED_PEAKS.json
+
+
+def predicted_time_b200(algo, s: MultiplySpec, machine: B200Machine = B200Machine()):
+    """Extension (not in the reference): seconds per multiply on
+    s.nprocs B200s joined by NVSwitch.  Volumes are the paper's (Eq. 1/2/5, in
+    elements); what differs from the volume argmin is how they meet the
+    compute:
+      * compute: 2*M*N*K*occ_a*occ_b useful flops split over the GPUs, plus the
+        C slab written once from HBM;
+      * Cannon: the shifts are posted before each local multiply, so time =
+        max(compute, traffic); only square grids;
+      * case 1: the C reduction follows the local multiply (not hidden);
+      * case 2 (B gather): the value transfer overlaps the symbolic passes only
+        (counted as half hidden).
+    Every GPU has the full NVLink bandwidth to every peer (NVSwitch), so
+    traffic time = bytes per rank / link bandwidth."""
+    s.validate()
+    p = s.nprocs
+    flops = 2.0 * s.m * s.n * s.k * s.occ_a * s.occ_b
+    compute = flops / (p * machine.fp64_flops) + 8.0 * s.stored_c() / p / machine.hbm_bytes
+    if algo == Algorithm.cannon:
+        q = round(math.sqrt(p))
+        if q * q != p:
+            return math.inf
+        return max(compute, 8.0 * cannon_volume(s) / machine.link_bytes)
+    if algo == Algorithm.case1:
+        return compute + 8.0 * case1_volume(s) / machine.link_bytes
+    if algo == Algorithm.case2:
+        return compute + 0.5 * 8.0 * case2_volume(s) / machine.link_bytes
+    raise InvalidArgument("predicted_time_b200: unknown algorithm")
+
+
+def select_algorithm_b200(m, n, k, occ_a, occ_b, occ_c_estimate, nprocs,
+                          machine: B200Machine = B200Machine()):
+    """argmin of predicted_time_b200, ties cannon > case1 > case2 (the
+    reference's tie order, multiply_rect.hpp:45-63)."""
+    s = MultiplySpec(m, n, k, occ_a, occ_b, occ_c_estimate, nprocs)
+    best, bt = Algorithm.cannon, predicted_time_b200(Algorithm.cannon, s, machine)
+    for algo in (Algorithm.case1, Algorithm.case2):
+        t = predicted_time_b200(algo, s, machine)
+        if t < bt:
+            best, bt = algo, t
+    return best
+
+
 def measured_spec(a: DistMatrix, b: DistMatrix, occ_c, nprocs):
     """multiply_rect.hpp:254-265."""
     return MultiplySpec(a.rows().total(), b.cols().total(), a.cols().total(), a.occupancy(),

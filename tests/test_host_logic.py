@@ -53,3 +53,22 @@ def test_mixed_radix_matches_oracle(oracle):
         c = t.mixed_radix_inv(idx, ext)
         assert t.mixed_radix(c, ext) == idx == oracle.mixed_radix(c, ext)
     assert t.mixed_radix([2, 3], [3, 4]) == 11   # SPEC.md:510 example
+
+
+@pytest.mark.parametrize("shape,p,want", [
+    # c5: dense-ish 65 536^3 at 50 %, square grid -> Cannon (shifts hidden)
+    ((65536, 65536, 65536, 0.5, 0.5, 1.0), 4, d.Algorithm.cannon),
+    # c5 on 8 GPUs: no square grid -> a rectangular algorithm
+    ((65536, 65536, 65536, 0.5, 0.5, 1.0), 8, d.Algorithm.case2),
+    # c3: C 2000^2 from K = 400 000 (S_C << S_A, S_B) -> case 1
+    ((2000, 2000, 400000, 0.1, 0.1, 1.0), 4, d.Algorithm.case1),
+    # c1 weak-scaling shape on 2 GPUs (non-square) -> case 2
+    ((9200 * 2, 9200, 9200, 0.1, 0.1, 0.98), 2, d.Algorithm.case2),
+])
+def test_b200_time_model_selection(shape, p, want):
+    """Extension: NVLink-aware selection picks the algorithm the
+    measurements favour for the BASELINE shapes."""
+    assert d.select_algorithm_b200(*shape, p) == want
+    s = d.MultiplySpec(*shape, p)
+    times = [d.predicted_time_b200(a, s) for a in (0, 1, 2)]
+    assert min(times) == d.predicted_time_b200(want, s)
