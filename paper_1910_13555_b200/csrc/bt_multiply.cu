@@ -637,16 +637,41 @@ KernelFn dmma_kernel_s(int cls) {
   return table[cls];
 }
 
+// one launch for all DMMA classes of a mixed-size multiply: the smallest
+// instantiation whose largest tile (TM x TN tiles of 8) covers every class
+KernelFn dmma_multi_kernel(int maxm, int maxn, int& cache_slot, int& plan_cls) {
+  if (maxm <= 3 && maxn <= 3) {
+    cache_slot = 16;
+    plan_cls = 10;
+    return k_smm_dmma<3, 3, kWarps, 1, true>;
+  }
+  if (maxn <= 3) {
+    cache_slot = 17;
+    plan_cls = 14;
+    return k_smm_dmma<4, 3, kWarps, 1, true>;
+  }
+  if (maxm <= 3) {
+    cache_slot = 18;
+    plan_cls = 11;
+    return k_smm_dmma<3, 4, kWarps, 1, true>;
+  }
+  cache_slot = 19;
+  plan_cls = 15;
+  return k_smm_dmma<4, 4, kWarps, 1, true>;
+}
+
 KernelFn dmma_kernel(int cls, int stages) {
   return stages >= 2 ? dmma_kernel_s<2>(cls) : dmma_kernel_s<1>(cls);
 }
 
 // cudaFuncSetAttribute + occupancy query, cached per (kernel, smem bytes)
 int dmma_occupancy(int cls, KernelFn fn, size_t smem) {
-  static KernelFn cached_fn[16] = {nullptr};
-  static size_t cached_smem[16] = {0};
-  static int cached_occ[16] = {0};
-  static int cached_dev[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+  // slots 0..15: per-class kernels; 16..19: the MULTI kernels
+  static KernelFn cached_fn[20] = {nullptr};
+  static size_t cached_smem[20] = {0};
+  static int cached_occ[20] = {0};
+  static int cached_dev[20] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
+                               -1, -1, -1, -1};
   int dev = 0;
   BT_CUDA(cudaGetDevice(&dev));
   if (cached_fn[cls] == fn && cached_smem[cls] == smem && cached_dev[cls] == dev)
@@ -946,18 +971,47 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       const int ktmax = std::max(1, tiles8(kmax));
       int nclasses = 0;
       for (int q = 0; q < NCLASS; ++q) nclasses += ibound[q + 1] > ibound[q];
-      // several classes (mixed block sizes): fork onto the side streams so the
-      // small per-class grids fill the GPU together
+      // several classes (mixed block sizes): all DMMA classes in ONE launch of
+      // the MULTI kernel (per-item tile dispatch; BT_MULTI=0: one kernel per
+      // class on side streams); the generic class beside it
+      int maxm = 0, maxn = 0;
+      for (int q = 0; q < GENERIC; ++q)
+        if (ibound[q + 1] > ibound[q]) {
+          maxm = std::max(maxm, q / 4 + 1);
+          maxn = std::max(maxn, q % 4 + 1);
+        }
+      const bool multi = nclasses > 1 && maxm > 0 && env_int("BT_MULTI", 1) != 0;
       const bool fork = nclasses > 1;
+      const int nstreams = std::min(nclasses, Ctx::kAux);
       if (fork) {
         BT_CUDA(cudaEventRecord(x.ev_fork, st));
-        for (auto& a : x.aux) BT_CUDA(cudaStreamWaitEvent(a, x.ev_fork, 0));
+        for (int a = 0; a < nstreams; ++a) BT_CUDA(cudaStreamWaitEvent(x.aux[a], x.ev_fork, 0));
       }
-      int launched = 0;
+      if (multi) {
+        int slot = 0, pcls = 0;
+        KernelFn fn = dmma_multi_kernel(maxm, maxn, slot, pcls);
+        const Plan P = plan_dmma(pcls, ktmax);  // stage plan of the largest tile
+        g.stages = 1;
+        g.stage_doubles = P.stage_doubles;
+        g.a_region = P.a_region;
+        const size_t smem = kWarps * 1536 + static_cast<size_t>(kWarps) * P.stage_doubles * 8;
+        g.item_lo = ibound[0];
+        g.nitems = ibound[GENERIC] - ibound[0];
+        g.counter = counters;  // class 0's ticket counter serves the single launch
+        const int per_sm = dmma_occupancy(slot, fn, smem);
+        BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
+        const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,
+                                               (g.nitems + kWarps - 1) / kWarps);
+        fn<<<static_cast<unsigned>(grid), kWarps * 32, smem, x.aux[0]>>>(g);
+        check_launch("smm_dmma_multi");
+        count_launch(&x);
+      }
+      int launched = multi ? 1 : 0;
       for (int q = 0; q < NCLASS; ++q) {
         const int64_t lo = ibound[q], hi = ibound[q + 1];
         if (hi <= lo) continue;
-        cudaStream_t ks = fork ? x.aux[launched % Ctx::kAux] : st;
+        if (multi && q != GENERIC) continue;
+        cudaStream_t ks = fork ? x.aux[launched % nstreams] : st;
         ++launched;
         g.item_lo = lo;
         g.nitems = hi - lo;
@@ -982,7 +1036,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         count_launch(&x);
       }
       if (fork)
-        for (int a = 0; a < Ctx::kAux; ++a) {
+        for (int a = 0; a < nstreams; ++a) {
           BT_CUDA(cudaEventRecord(x.ev_join[a], x.aux[a]));
           BT_CUDA(cudaStreamWaitEvent(st, x.ev_join[a], 0));
         }

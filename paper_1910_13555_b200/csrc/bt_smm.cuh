@@ -17,6 +17,8 @@
 //    order.
 #pragma once
 
+#include <type_traits>
+
 #include "bt_internal.cuh"
 #include "bt_ptx.cuh"
 
@@ -77,7 +79,11 @@ template <int TMT, int TNT>
 constexpr int dmma_min_blocks() {
   return TMT * TNT <= 9 ? 5 : 3;
 }
-template <int TMT, int TNT, int WARPS, int S>
+// MULTI: one launch for every DMMA class of a mixed-size multiply -- TMT x TNT
+// is then the largest tile, each item's own tile shape comes from its rows and
+// columns, and the consumer dispatches to the matching instantiation of the
+// tile body (so small classes do not pay for the large accumulators).
+template <int TMT, int TNT, int WARPS, int S, bool MULTI = false>
 __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_smm_dmma(const NumArgs g) {
   constexpr int QN = 8;     // item slots per warp
   constexpr int CTL = 1536; // control block bytes per warp
@@ -136,6 +142,7 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
   int qh = 0, qt = 0;  // consumer / producer item sequence numbers
   int64_t p_pos = 0, p_end = 0;
   int p_r8 = 0, p_mt = 0;
+  int p_nt = TNT;  // B tile columns of the item being issued (MULTI: per item)
   bool p_more = true;
 
   // next chunk after (item seq n, desc index pos) -- returns false if unknown yet
@@ -209,6 +216,7 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         p_end = p_pos + it.np;
         p_r8 = item_r8(it);
         p_mt = (it.rows + 7) >> 3;
+        if constexpr (MULTI) p_nt = (it.n + 7) >> 3;
         ++qt;
         if (p_pos < p_end) enter_chunk(qt - 1, p_pos, p_end);
         continue;
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         const Desc d = dring[cs * 32 + static_cast<int>(p_pos - c_base)];
         const int KT = (d.z + 1) >> 1;  // 8-wide k tiles
         const uint32_t ba = static_cast<uint32_t>(p_mt * KT) * 512u;
-        const uint32_t bb = static_cast<uint32_t>(KT * TNT) * 512u;
+        const uint32_t bb = static_cast<uint32_t>(KT * p_nt) * 512u;
         double* st = stages + static_cast<int64_t>(s) * g.stage_doubles;
         stage_kc[s] = d.z;
         fence_proxy_async_smem();
@@ -247,84 +255,107 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
       __syncwarp();
       continue;
     }
-    double acc[TMT][TNT][2];
+    // the tile body for a CM x CN tile (8-row x 8-column DMMA tiles)
+    auto tile = [&](auto cm_c, auto cn_c) {
+      constexpr int CM = decltype(cm_c)::value, CN = decltype(cn_c)::value;
+      double acc[CM][CN][2];
 #pragma unroll
-    for (int tm = 0; tm < TMT; ++tm)
+      for (int tm = 0; tm < CM; ++tm)
 #pragma unroll
-      for (int tn = 0; tn < TNT; ++tn) {
-        acc[tm][tn][0] = 0.0;
-        acc[tm][tn][1] = 0.0;
+        for (int tn = 0; tn < CN; ++tn) {
+          acc[tm][tn][0] = 0.0;
+          acc[tm][tn][1] = 0.0;
+        }
+      if (it.cin_off >= 0) {
+#pragma unroll
+        for (int tm = 0; tm < CM; ++tm)
+          if (tm < mt) {
+#pragma unroll
+            for (int tn = 0; tn < CN; ++tn) {
+              const double2 v = *reinterpret_cast<const double2*>(
+                  g.cin + it.cin_off + ((tm * CN + tn) << 6) + lc);
+              acc[tm][tn][0] = v.x;
+              acc[tm][tn][1] = v.y;
+            }
+          }
       }
-    if (it.cin_off >= 0) {
+      for (int t = 0; t < it.np; ++t) {
+        const int s = s_cons;
+        mbar_wait(&bars[s], cons_phase);
+        if (++s_cons == S) {
+          s_cons = 0;
+          cons_phase ^= 1u;
+        }
+        const int kc = stage_kc[s];
+        const int KT = (kc + 1) >> 1;
+        const double* sA = stages + static_cast<int64_t>(s) * g.stage_doubles;
+        const double* sB = sA + g.a_region;
+        // k tiles, unrolled by 4 with uniform guards (KT <= 8 for DMMA classes)
+        for (int kt0 = 0; kt0 < KT; kt0 += 4) {
 #pragma unroll
-      for (int tm = 0; tm < TMT; ++tm)
+          for (int u = 0; u < 4; ++u) {
+            const int kt = kt0 + u;
+            if (kt < KT) {
+              // two 4-wide k chunks per 8x8 tile column (the second may be padding)
+              double af[2][CM], bf[2][CN];
+#pragma unroll
+              for (int tm = 0; tm < CM; ++tm) {
+                af[0][tm] = sA[((tm * KT + kt) << 6) + la0];
+                af[1][tm] = sA[((tm * KT + kt) << 6) + la1];
+              }
+#pragma unroll
+              for (int tn = 0; tn < CN; ++tn) {
+                bf[0][tn] = sB[((kt * CN + tn) << 6) + lb0];
+                bf[1][tn] = sB[((kt * CN + tn) << 6) + lb1];
+              }
+#pragma unroll
+              for (int tm = 0; tm < CM; ++tm)
+#pragma unroll
+                for (int tn = 0; tn < CN; ++tn)
+                  dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[0][tm], bf[0][tn]);
+              if (2 * kt + 1 < kc) {
+#pragma unroll
+                for (int tm = 0; tm < CM; ++tm)
+#pragma unroll
+                  for (int tn = 0; tn < CN; ++tn)
+                    dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[1][tm], bf[1][tn]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        ++consumed;
+        top_up();
+      }
+      double* dst = g.cout + it.c_off;
+#pragma unroll
+      for (int tm = 0; tm < CM; ++tm)
         if (tm < mt) {
 #pragma unroll
-          for (int tn = 0; tn < TNT; ++tn) {
-            const double2 v = *reinterpret_cast<const double2*>(
-                g.cin + it.cin_off + ((tm * TNT + tn) << 6) + lc);
-            acc[tm][tn][0] = v.x;
-            acc[tm][tn][1] = v.y;
-          }
+          for (int tn = 0; tn < CN; ++tn)
+            __stcs(reinterpret_cast<double2*>(dst + ((tm * CN + tn) << 6) + lc),
+                   make_double2(acc[tm][tn][0], acc[tm][tn][1]));
         }
+    };
+    if constexpr (MULTI) {
+      const int cls = (mt - 1) * 4 + (((it.n + 7) >> 3) - 1);
+      using std::integral_constant;
+#define BT_TILE(cm, cn)                                                   \
+  case (cm - 1) * 4 + (cn - 1):                                           \
+    if constexpr (cm <= TMT && cn <= TNT)                                 \
+      tile(integral_constant<int, cm>{}, integral_constant<int, cn>{});   \
+    break;
+      switch (cls) {
+        BT_TILE(1, 1) BT_TILE(1, 2) BT_TILE(1, 3) BT_TILE(1, 4)
+        BT_TILE(2, 1) BT_TILE(2, 2) BT_TILE(2, 3) BT_TILE(2, 4)
+        BT_TILE(3, 1) BT_TILE(3, 2) BT_TILE(3, 3) BT_TILE(3, 4)
+        BT_TILE(4, 1) BT_TILE(4, 2) BT_TILE(4, 3) BT_TILE(4, 4)
+        default: break;
+      }
+#undef BT_TILE
+    } else {
+      tile(std::integral_constant<int, TMT>{}, std::integral_constant<int, TNT>{});
     }
-    for (int t = 0; t < it.np; ++t) {
-      const int s = s_cons;
-      mbar_wait(&bars[s], cons_phase);
-      if (++s_cons == S) {
-        s_cons = 0;
-        cons_phase ^= 1u;
-      }
-      const int kc = stage_kc[s];
-      const int KT = (kc + 1) >> 1;
-      const double* sA = stages + static_cast<int64_t>(s) * g.stage_doubles;
-      const double* sB = sA + g.a_region;
-      // k tiles, unrolled by 4 with uniform guards (KT <= 8 for DMMA classes)
-      for (int kt0 = 0; kt0 < KT; kt0 += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int kt = kt0 + u;
-          if (kt < KT) {
-            // two 4-wide k chunks per 8x8 tile column (the second may be padding)
-            double af[2][TMT], bf[2][TNT];
-#pragma unroll
-            for (int tm = 0; tm < TMT; ++tm) {
-              af[0][tm] = sA[((tm * KT + kt) << 6) + la0];
-              af[1][tm] = sA[((tm * KT + kt) << 6) + la1];
-            }
-#pragma unroll
-            for (int tn = 0; tn < TNT; ++tn) {
-              bf[0][tn] = sB[((kt * TNT + tn) << 6) + lb0];
-              bf[1][tn] = sB[((kt * TNT + tn) << 6) + lb1];
-            }
-#pragma unroll
-            for (int tm = 0; tm < TMT; ++tm)
-#pragma unroll
-              for (int tn = 0; tn < TNT; ++tn)
-                dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[0][tm], bf[0][tn]);
-            if (2 * kt + 1 < kc) {
-#pragma unroll
-              for (int tm = 0; tm < TMT; ++tm)
-#pragma unroll
-                for (int tn = 0; tn < TNT; ++tn)
-                  dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[1][tm], bf[1][tn]);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      ++consumed;
-      top_up();
-    }
-    double* dst = g.cout + it.c_off;
-#pragma unroll
-    for (int tm = 0; tm < TMT; ++tm)
-      if (tm < mt) {
-#pragma unroll
-        for (int tn = 0; tn < TNT; ++tn)
-          __stcs(reinterpret_cast<double2*>(dst + ((tm * TNT + tn) << 6) + lc),
-                 make_double2(acc[tm][tn][0], acc[tm][tn][1]));
-      }
     ++qh;
     top_up();
     __syncwarp();
