@@ -155,8 +155,13 @@ __device__ __forceinline__ int find_entry(const RowChunk& rc, int n, int32_t t) 
 // cnt[j]: products of C(i,j) (kept by the eps filter) | kCinFlag for C_in blocks;
 // bits[j/32]: column j touched.  The column passes then visit touched columns
 // only (word by word), so their cost is O(N/32 + touched) per row.
-__device__ void row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_t* bits,
-                             RowChunk& rc, unsigned long long* cand, unsigned long long* mnk) {
+// cache_j / cache_bu (fill pass, optional): for a row that is one chunk of
+// at most kPairCap pairs, pair t's column (0xffffffff if filtered out) and B
+// tile offset are kept in shared memory so the emission sweeps need no global
+// loads; returns whether the cache is valid.
+__device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_t* bits,
+                             RowChunk& rc, unsigned long long* cand, unsigned long long* mnk,
+                             uint32_t* cache_j = nullptr, int32_t* cache_bu = nullptr) {
   const int nw = static_cast<int>((g.ncols + 31) >> 5);
   for (int64_t j = threadIdx.x; j < g.ncols; j += blockDim.x) cnt[j] = 0u;
   for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0u;
@@ -167,20 +172,31 @@ __device__ void row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
     atomicOr(&bits[j >> 5], 1u << (j & 31));
   }
   const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
+  bool cached = false;
   for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
     const int n = min(kChunkA, a1 - c0);
     const int64_t T = stage_chunk(g, c0, a1, rc);
+    const bool cache = cache_j && a1 - a0 <= kChunkA && T <= kPairCap;
     for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
       const int l = find_entry(rc, n, static_cast<int32_t>(t));
       const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
       if (cand) ++*cand;
-      if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
+      if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) {
+        if (cache) cache_j[t] = 0xffffffffu;
+        continue;
+      }
       const int32_t j = g.b_col[f];
+      if (cache) {
+        cache_j[t] = static_cast<uint32_t>(j);
+        cache_bu[t] = static_cast<int32_t>(g.b_off[f] >> 6);
+      }
       if (atomicAdd(&cnt[j], 1u) == 0u) atomicOr(&bits[j >> 5], 1u << (j & 31));
       if (mnk) *mnk += static_cast<unsigned long long>(rc.ksz[l]) * g.n_sz[j];
     }
     __syncthreads();
+    cached = cache;
   }
+  return cached;
 }
 
 // Warp-aggregated shared-memory atomicAdd: lanes adding to the same counter
@@ -293,7 +309,8 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   __shared__ unsigned long long cls_n[NSEG], cls_at[NSEG];
   const int64_t i = blockIdx.x;
   for (int t = threadIdx.x; t < NSEG; t += blockDim.x) cls_n[t] = 0;
-  row_products(g, i, cnt, bits, rc, nullptr, nullptr);
+  // single-chunk rows: pair columns / B offsets cached, rc stays staged
+  const bool cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, s_key, s_bu);
   const int m = g.m_sz[i];
   const int32_t cbase = g.out_rp[i];
   const int64_t pbase = g.prod_base[i], vbase = g.val_base[i];
@@ -373,7 +390,35 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
   for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
     const int n = min(kChunkA, a1 - c0);
-    const int64_t T = stage_chunk(g, c0, a1, rc);
+    const int64_t T = cached ? rc.pref[n] : stage_chunk(g, c0, a1, rc);
+    if (cached && g.colmask && n <= 64) {
+      // rank emission from the cached pairs (no global loads in the sweeps)
+      unsigned long long* mask = reinterpret_cast<unsigned long long*>(
+          sm + ((3 * g.ncols + ((g.ncols + 31) >> 5) + 1) & ~int64_t(1)));
+      for (int q = threadIdx.x; q < ntouch; q += blockDim.x) mask[tcol[q]] = 0ull;
+      __syncthreads();
+      for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint32_t j = s_key[t];
+        if (j == 0xffffffffu) continue;
+        const int l = find_entry(rc, n, static_cast<int32_t>(t));
+        atomicOr(&mask[j], 1ull << l);
+      }
+      __syncthreads();
+      for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint32_t j = s_key[t];
+        if (j == 0xffffffffu) continue;
+        const int l = find_entry(rc, n, static_cast<int32_t>(t));
+        const int32_t p = cur[j] + __popcll(mask[j] & ((1ull << l) - 1ull));
+        g.desc[pbase + p] = make_int4(rc.au[l], s_bu[t], (rc.ksz[l] + 3) >> 2, rc.k[l]);
+      }
+      __syncthreads();
+      for (int q = threadIdx.x; q < ntouch; q += blockDim.x) {
+        const int j = tcol[q];
+        cur[j] += __popcll(mask[j]);
+      }
+      __syncthreads();
+      continue;
+    }
     if (g.colmask && n <= 64) {
       // Rank emission (chunks of <= 64 A entries): bit l of mask[j] marks the
       // pair (A entry l, column j); a pair's slot in its C block is cur[j] +
