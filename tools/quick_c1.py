@@ -1,23 +1,24 @@
-"""Quick timing of the local multiply on BASELINE config 1 (dev tool)."""
+"""Quick timing of the local multiply on a c1-like shape (dev tool):
+  python tools/quick_c1.py [block_size] [n_blocks] [occupancy]
+Inputs: bench.make_blocks (numpy PCG64, seeds 1001/1002)."""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
-from oracle.oracle import Oracle
+import bench
 from paper_1910_13555_b200.store import Context, LocalStore, multiply_local
 
-o = Oracle()
 bs = int(sys.argv[1]) if len(sys.argv) > 1 else 23
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else 400
 occ = float(sys.argv[3]) if len(sys.argv) > 3 else 0.10
 sz = np.full(nb, bs, np.int32)
 t = time.time()
-A = o.random_matrix(1001, sz, sz, occ)
-B = o.random_matrix(1002, sz, sz, occ)
-print("gen", time.time() - t, A.nblk, B.nblk, flush=True)
+abi, abj, av = bench.make_blocks(bench.SEED_A, nb, nb, bs, occ)
+bbi, bbj, bv = bench.make_blocks(bench.SEED_B, nb, nb, bs, occ)
+print("gen", time.time() - t, len(abi), len(bbi), flush=True)
 ctx = Context(0)
 ctx.set_timing(True)
-a = LocalStore(ctx, sz, sz); a.put_blocks(A.bi, A.bj, A.vals)
-b = LocalStore(ctx, sz, sz); b.put_blocks(B.bi, B.bj, B.vals)
+a = LocalStore(ctx, sz, sz); a.put_blocks(abi, abj, av)
+b = LocalStore(ctx, sz, sz); b.put_blocks(bbi, bbj, bv)
 c = LocalStore(ctx, sz, sz)
 for it in range(8):
     c.clear(); ctx.sync()
