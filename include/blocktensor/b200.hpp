@@ -12,6 +12,7 @@
 //                         process's GPU (or, via SimComm::nccl, one rank per process)
 //   matrix.hpp:26-418     Axis, DistMatrix, new_matrix, new_matrix_round_robin
 //   multiply_cannon.hpp   multiply_cannon
+//   (SPEC tensor module) SparseTensor, contract, mixed_radix
 //   multiply_rect.hpp     Algorithm, multiply_reduce_case1, multiply_virtual_case2,
 //                         multiply_dispatch, select_algorithm, measured_spec
 //   cost_model.hpp        MultiplySpec + Eq. 1-5
@@ -622,6 +623,221 @@ inline MultiplySpec measured_spec(const DistMatrix& a, const DistMatrix& b, doub
   s.occ_c = occ_c;
   s.nprocs = nprocs;
   return s;
+}
+
+
+// ------------------------------------------------------------------ tensors
+// SPEC.md:479-545 (the tensor module exists only in the reference's spec):
+// block-sparse tensors of rank 2..4 stored as a device matrix under a
+// matricization map (row-group dims | col-group dims), mixed radix with later
+// dimensions fastest for block indices and for the elements inside a block
+// (SPEC.md:505-513, 533).  Mirror of paper_1910_13555_b200/tensor.py; the
+// index remap runs on the device (bt_tensor_remap), the contraction through
+// the block-sparse multiply (bt_multiply).
+inline std::int64_t mixed_radix(const std::vector<std::int64_t>& coords,
+                                const std::vector<std::int64_t>& extents) {
+  if (coords.size() != extents.size()) throw invalid_argument("mixed_radix: rank mismatch");
+  std::int64_t idx = 0;
+  for (std::size_t d = 0; d < coords.size(); ++d) {
+    if (coords[d] < 0 || coords[d] >= extents[d])
+      throw invalid_argument("tensor index out of range");
+    idx = idx * extents[d] + coords[d];
+  }
+  return idx;
+}
+
+class SparseTensor {
+ public:
+  SparseTensor(SimComm& comm, std::vector<Blocking> dims, std::vector<int> row_dims,
+               std::vector<int> col_dims)
+      : ctx_(comm.context()), dims_(std::move(dims)), row_(std::move(row_dims)),
+        col_(std::move(col_dims)) {
+    const int n = static_cast<int>(dims_.size());
+    if (n < 2 || n > 4) throw invalid_argument("tensor: rank must be in [2, 4]");
+    std::vector<int> all(row_);
+    all.insert(all.end(), col_.begin(), col_.end());
+    std::vector<int> sorted_all(all);
+    std::sort(sorted_all.begin(), sorted_all.end());
+    for (int d = 0; d < n; ++d)
+      if (static_cast<int>(sorted_all.size()) != n || sorted_all[d] != d || row_.empty() ||
+          col_.empty())
+        throw invalid_argument(
+            "tensor: map is not a partition of the dimensions into two non-empty groups");
+    const std::vector<int> rs = group_sizes(row_), cs = group_sizes(col_);
+    detail::check(bt_mat_create(ctx_, static_cast<std::int64_t>(rs.size()), rs.data(),
+                                static_cast<std::int64_t>(cs.size()), cs.data(), &m_));
+  }
+  SparseTensor(const SparseTensor&) = delete;
+  SparseTensor& operator=(const SparseTensor&) = delete;
+  SparseTensor(SparseTensor&& o) noexcept
+      : ctx_(o.ctx_), dims_(std::move(o.dims_)), row_(std::move(o.row_)),
+        col_(std::move(o.col_)), m_(o.m_) {
+    o.m_ = nullptr;
+  }
+  ~SparseTensor() {
+    if (m_) bt_mat_destroy(m_);
+  }
+
+  int rank() const noexcept { return static_cast<int>(dims_.size()); }
+  const std::vector<Blocking>& dims() const noexcept { return dims_; }
+  const std::vector<int>& row_dims() const noexcept { return row_; }
+  const std::vector<int>& col_dims() const noexcept { return col_; }
+  bt_mat* store() const noexcept { return m_; }
+
+  // tensor_to_matrix_index
+  std::pair<std::int64_t, std::int64_t> to_matrix_index(
+      const std::vector<std::int64_t>& coords) const {
+    if (static_cast<int>(coords.size()) != rank()) throw invalid_argument("tensor: rank mismatch");
+    return {group_index(row_, coords), group_index(col_, coords)};
+  }
+  std::vector<int> block_shape(const std::vector<std::int64_t>& coords) const {
+    std::vector<int> sh(dims_.size());
+    for (std::size_t d = 0; d < dims_.size(); ++d) sh[d] = dims_[d].size(coords[d]);
+    return sh;
+  }
+  // values row-major over the tensor dimensions (dimension 0 slowest)
+  void put_block(const std::vector<std::int64_t>& coords, const std::vector<double>& values,
+                 bool accumulate = false) {
+    const auto sh = block_shape(coords);
+    std::int64_t n = 1;
+    for (int s : sh) n *= s;
+    if (static_cast<std::int64_t>(values.size()) != n)
+      throw invalid_argument("tensor put_block: value count does not match the block shape");
+    const auto ij = to_matrix_index(coords);
+    const std::vector<double> mat = permute(values, sh, order(), false);
+    const std::int64_t i = ij.first, j = ij.second;
+    const double* v = mat.data();
+    detail::check(bt_mat_put_blocks(m_, 1, &i, &j, v, accumulate ? 1 : 0));
+  }
+  bool get_block(const std::vector<std::int64_t>& coords, std::vector<double>& out) const {
+    const auto sh = block_shape(coords);
+    std::int64_t n = 1;
+    for (int s : sh) n *= s;
+    std::vector<double> mat(static_cast<std::size_t>(n));
+    const auto ij = to_matrix_index(coords);
+    int found = 0;
+    detail::check(bt_mat_get_block(m_, ij.first, ij.second, mat.data(), &found));
+    if (!found) return false;
+    out = permute(mat, sh, order(), true);
+    return true;
+  }
+  // the same tensor under another map (device remap kernel)
+  SparseTensor remap(SimComm& comm, std::vector<int> row_dims, std::vector<int> col_dims) const {
+    SparseTensor out(comm, dims_, row_dims, col_dims);
+    std::vector<std::int64_t> nb(dims_.size());
+    std::vector<std::vector<std::int32_t>> sz(dims_.size());
+    std::vector<const std::int32_t*> szp(dims_.size());
+    for (std::size_t d = 0; d < dims_.size(); ++d) {
+      nb[d] = dims_[d].n_blocks();
+      for (std::int64_t b = 0; b < nb[d]; ++b) sz[d].push_back(dims_[d].size(b));
+      szp[d] = sz[d].data();
+    }
+    std::vector<int> src(row_), dst(row_dims);
+    src.insert(src.end(), col_.begin(), col_.end());
+    dst.insert(dst.end(), col_dims.begin(), col_dims.end());
+    detail::check(bt_tensor_remap(ctx_, rank(), nb.data(), szp.data(),
+                                  static_cast<int>(row_.size()), src.data(), m_,
+                                  static_cast<int>(row_dims.size()), dst.data(), out.m_));
+    return out;
+  }
+
+ private:
+  std::vector<int> order() const {
+    std::vector<int> o(row_);
+    o.insert(o.end(), col_.begin(), col_.end());
+    return o;
+  }
+  std::vector<int> group_sizes(const std::vector<int>& g) const {
+    std::vector<int> out{1};
+    for (int d : g) {
+      std::vector<int> nx;
+      for (int a : out)
+        for (std::int64_t b = 0; b < dims_[d].n_blocks(); ++b) nx.push_back(a * dims_[d].size(b));
+      out.swap(nx);
+    }
+    return out;
+  }
+  std::int64_t group_index(const std::vector<int>& g, const std::vector<std::int64_t>& c) const {
+    std::vector<std::int64_t> cc, ext;
+    for (int d : g) {
+      cc.push_back(c[d]);
+      ext.push_back(dims_[d].n_blocks());
+    }
+    return mixed_radix(cc, ext);
+  }
+  // tensor-order values <-> matrix-order values (axes permuted by `perm`)
+  static std::vector<double> permute(const std::vector<double>& in, const std::vector<int>& sh,
+                                     const std::vector<int>& perm, bool inverse) {
+    const int n = static_cast<int>(sh.size());
+    std::vector<std::int64_t> tstride(n), pstride(n);
+    std::int64_t s = 1;
+    for (int d = n - 1; d >= 0; --d) {
+      tstride[d] = s;
+      s *= sh[d];
+    }
+    s = 1;
+    for (int q = n - 1; q >= 0; --q) {  // stride of tensor dim perm[q] in permuted order
+      pstride[perm[q]] = s;
+      s *= sh[perm[q]];
+    }
+    std::vector<double> out(in.size());
+    std::vector<int> idx(n, 0);
+    for (std::int64_t t = 0; t < static_cast<std::int64_t>(in.size()); ++t) {
+      std::int64_t to = 0, po = 0;
+      for (int d = 0; d < n; ++d) {
+        to += idx[d] * tstride[d];
+        po += idx[d] * pstride[d];
+      }
+      if (inverse) out[to] = in[po]; else out[po] = in[to];
+      for (int d = n - 1; d >= 0; --d) {
+        if (++idx[d] < sh[d]) break;
+        idx[d] = 0;
+      }
+    }
+    return out;
+  }
+
+  bt_ctx* ctx_ = nullptr;
+  std::vector<Blocking> dims_;
+  std::vector<int> row_, col_;
+  bt_mat* m_ = nullptr;
+};
+
+// contract: C += sum over (A dims ca) == (B dims cb) of A * B.
+// C's dimensions are A's retained dimensions (ascending) then B's.  Operands in
+// compatible maps are used as they are; others are remapped on the device
+// first, and C is remapped back to its own map.
+inline void contract(SimComm& comm, const SparseTensor& a, const SparseTensor& b,
+                     const std::vector<int>& ca, const std::vector<int>& cb, SparseTensor& c,
+                     double eps = 0.0) {
+  if (ca.size() != cb.size() || ca.empty())
+    throw invalid_argument("contract: contracted index lists must be non-empty and equal in length");
+  for (std::size_t q = 0; q < ca.size(); ++q)
+    if (!(a.dims()[ca[q]].sizes() == b.dims()[cb[q]].sizes()))
+      throw invalid_argument("contract: blockings of contracted indices differ");
+  std::vector<int> ra, rb;
+  for (int d = 0; d < a.rank(); ++d)
+    if (std::find(ca.begin(), ca.end(), d) == ca.end()) ra.push_back(d);
+  for (int d = 0; d < b.rank(); ++d)
+    if (std::find(cb.begin(), cb.end(), d) == cb.end()) rb.push_back(d);
+  if (c.rank() != static_cast<int>(ra.size() + rb.size()))
+    throw invalid_argument("contract: C rank does not match the retained indices");
+  std::vector<int> crow, ccol;
+  for (int q = 0; q < c.rank(); ++q) (q < static_cast<int>(ra.size()) ? crow : ccol).push_back(q);
+  const bool a_ok = a.row_dims() == ra && a.col_dims() == ca;
+  const bool b_ok = b.row_dims() == cb && b.col_dims() == rb;
+  const bool c_ok = c.row_dims() == crow && c.col_dims() == ccol;
+  std::unique_ptr<SparseTensor> am, bm, cm;
+  if (!a_ok) am.reset(new SparseTensor(a.remap(comm, ra, ca)));
+  if (!b_ok) bm.reset(new SparseTensor(b.remap(comm, cb, rb)));
+  if (!c_ok) cm.reset(new SparseTensor(c.remap(comm, crow, ccol)));
+  bt_stats st{};
+  detail::check(bt_multiply(comm.context(), am ? am->store() : a.store(),
+                            bm ? bm->store() : b.store(), cm ? cm->store() : c.store(), eps, &st));
+  if (!c_ok) {
+    SparseTensor back = cm->remap(comm, c.row_dims(), c.col_dims());
+    detail::check(bt_mat_copy(back.store(), c.store()));
+  }
 }
 
 }  // namespace blocktensor

@@ -54,3 +54,20 @@ def test_facade_maps_errors(tmp_path, oracle):
     write_matrix_binary(paths[2], A)
     r = subprocess.run([EXE, "cannon", "1", "1"] + paths, capture_output=True, text=True)
     assert r.returncode == 1 and "inner blockings" in r.stderr
+
+
+def test_facade_tensor_example_compiles():
+    _build()
+    assert os.path.exists(os.path.join(ROOT, "examples", "contract_tensor"))
+
+
+@pytest.mark.gpu
+def test_facade_tensor_contraction():
+    """C++ SparseTensor / contract through the C-ABI: the
+    rank-3 (ab|P)(P|Q) contraction with a device remap of T, vs a dense host
+    evaluation inside the example (exit 0 iff <= 1e-12)."""
+    _build()
+    r = subprocess.run([os.path.join(ROOT, "examples", "contract_tensor")], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "frobenius rel err" in r.stdout
