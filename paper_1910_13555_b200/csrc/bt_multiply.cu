@@ -16,6 +16,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <tuple>
+#include <mutex>
+#include <map>
 #include <array>
 #include <cstdlib>
 
@@ -684,23 +687,19 @@ KernelFn dmma_kernel_s(int cls) {
 
 // one launch for all DMMA classes of a mixed-size multiply: the smallest
 // instantiation whose largest tile (TM x TN tiles of 8) covers every class
-KernelFn dmma_multi_kernel(int maxm, int maxn, int& cache_slot, int& plan_cls) {
+KernelFn dmma_multi_kernel(int maxm, int maxn, int& plan_cls) {
   if (maxm <= 3 && maxn <= 3) {
-    cache_slot = 16;
     plan_cls = 10;
     return k_smm_dmma<3, 3, kWarps, 1, true>;
   }
   if (maxn <= 3) {
-    cache_slot = 17;
     plan_cls = 14;
     return k_smm_dmma<4, 3, kWarps, 1, true>;
   }
   if (maxm <= 3) {
-    cache_slot = 18;
     plan_cls = 11;
     return k_smm_dmma<3, 4, kWarps, 1, true>;
   }
-  cache_slot = 19;
   plan_cls = 15;
   return k_smm_dmma<4, 4, kWarps, 1, true>;
 }
@@ -709,26 +708,39 @@ KernelFn dmma_kernel(int cls, int stages) {
   return stages >= 2 ? dmma_kernel_s<2>(cls) : dmma_kernel_s<1>(cls);
 }
 
-// cudaFuncSetAttribute + occupancy query, cached per (kernel, smem bytes)
-int dmma_occupancy(int cls, KernelFn fn, size_t smem) {
-  // slots 0..15: per-class kernels; 16..19: the MULTI kernels
-  static KernelFn cached_fn[20] = {nullptr};
-  static size_t cached_smem[20] = {0};
-  static int cached_occ[20] = {0};
-  static int cached_dev[20] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
-                               -1, -1, -1, -1};
+// Dynamic shared-memory opt-in per (device, kernel): the largest size set so
+// far, raised when a launch needs more.  Thread-safe (one context per host
+// thread may drive its own device).
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, size_t> g_smem_set;
+std::map<std::tuple<int, const void*, size_t>, int> g_occ;
+
+void ensure_dyn_smem(const void* fn, size_t bytes) {
   int dev = 0;
   BT_CUDA(cudaGetDevice(&dev));
-  if (cached_fn[cls] == fn && cached_smem[cls] == smem && cached_dev[cls] == dev)
-    return cached_occ[cls];
-  cached_fn[cls] = fn;
-  BT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  size_t& cur = g_smem_set[{dev, fn}];
+  if (bytes > cur) {
+    BT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+    cur = bytes;
+  }
+}
+
+// opt-in + occupancy query of a numeric kernel, cached per (device, kernel, smem)
+int dmma_occupancy(KernelFn fn, size_t smem) {
+  ensure_dyn_smem(reinterpret_cast<const void*>(fn), smem);
+  int dev = 0;
+  BT_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_occ.find({dev, reinterpret_cast<const void*>(fn), smem});
+    if (it != g_occ.end()) return it->second;
+  }
   int per_sm = 0;
   BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWarps * 32, smem));
-  cached_smem[cls] = smem;
-  cached_occ[cls] = per_sm;
-  cached_dev[cls] = dev;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  g_occ[{dev, reinterpret_cast<const void*>(fn), smem}] = per_sm;
   return per_sm;
 }
 
@@ -866,12 +878,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     if (M > 0) {
       const size_t sm1 = static_cast<size_t>(N) * 8 + 4 * ((N + 31) / 32);
       // static + dynamic shared memory may exceed the 48 KB default: always opt in
-      static size_t set1 = 0;
-      if (sm1 > set1) {
-        BT_CUDA(cudaFuncSetAttribute(k_row_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(sm1)));
-        set1 = sm1;
-      }
+      ensure_dyn_smem(reinterpret_cast<const void*>(k_row_count), sm1);
       k_row_count<<<static_cast<unsigned>(M), kChunkA, sm1, st>>>(ra);
       check_launch("row_count");
       count_launch(&x);
@@ -947,12 +954,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.items = items;
     if (phases) BT_CUDA(cudaEventRecord(x.ev[5], st));
     if (nout > 0) {
-      static size_t set2 = 0;
-      if (row_smem > set2) {
-        BT_CUDA(cudaFuncSetAttribute(k_row_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(row_smem)));
-        set2 = row_smem;
-      }
+      ensure_dyn_smem(reinterpret_cast<const void*>(k_row_fill), row_smem);
       k_row_fill<<<static_cast<unsigned>(M), kChunkA, row_smem, st>>>(ra);
       check_launch("row_fill");
       count_launch(&x);
@@ -1033,8 +1035,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         for (int a = 0; a < nstreams; ++a) BT_CUDA(cudaStreamWaitEvent(x.aux[a], x.ev_fork, 0));
       }
       if (multi) {
-        int slot = 0, pcls = 0;
-        KernelFn fn = dmma_multi_kernel(maxm, maxn, slot, pcls);
+        int pcls = 0;
+        KernelFn fn = dmma_multi_kernel(maxm, maxn, pcls);
         const Plan P = plan_dmma(pcls, ktmax);  // stage plan of the largest tile
         g.stages = 1;
         g.stage_doubles = P.stage_doubles;
@@ -1043,7 +1045,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         g.item_lo = ibound[0];
         g.nitems = ibound[GENERIC] - ibound[0];
         g.counter = counters;  // class 0's ticket counter serves the single launch
-        const int per_sm = dmma_occupancy(slot, fn, smem);
+        const int per_sm = dmma_occupancy(fn, smem);
         BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
         const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,
                                                (g.nitems + kWarps - 1) / kWarps);
@@ -1072,7 +1074,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         g.stage_doubles = P.stage_doubles;
         g.a_region = P.a_region;
         KernelFn fn = dmma_kernel(q, P.stages);
-        const int per_sm = dmma_occupancy(q, fn, P.smem);
+        const int per_sm = dmma_occupancy(fn, P.smem);
         BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
         const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,
                                                (hi - lo + kWarps - 1) / kWarps);
