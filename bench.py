@@ -80,6 +80,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("BT_BENCH_NO_SMI"):  # diagnosis only: no sampler
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
