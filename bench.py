@@ -39,9 +39,9 @@ NB, BS, OCC = 400, 23, 0.10
 SEED_A, SEED_B = 1001, 1002
 FP64_PEAK_TFLOPS = 37.1   # measured: tools/microbench/fp64_peak.cu on B200 (profiles/)
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_smm_dmma launch on this
-# workload, from `ncu --set full` of this bench (profiles/r01b_ncu_dmma_bench_raw.csv):
-# 0.602 GB read + 0.696 GB written (algorithmic: 0.80 GB)
-NCU_TRAFFIC_BYTES = 1.298e9
+# workload, from `ncu --set full` of this bench (profiles/r01_final/ncu_dmma_bench_raw.csv):
+# 0.620 GB read + 0.695 GB written (algorithmic: 0.80 GB)
+NCU_TRAFFIC_BYTES = 1.316e9
 
 
 # --------------------------------------------------------------- inputs
@@ -358,6 +358,9 @@ def main():
             d2h = 8 * int(c.local(rank).info()[1]) + 16 * len(ci)
         if s >= args.warmup:
             e2e_times.append(dt)
+    if os.environ.get("BT_BENCH_DEBUG"):
+        print(f"[rank {rank}] e2e_ms {np.round(np.array(e2e_times) * 1e3, 2).tolist()}",
+              file=sys.stderr, flush=True)
     e2e_s = float(np.mean(e2e_times))
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64)
@@ -400,7 +403,7 @@ def main():
             "gpu_launches": int(kernels),
             "clocks": clocks.summary(),
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # rank 0 at N = 1 only
             cb, _ = cpu_baseline_sample()
             line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)
