@@ -187,3 +187,73 @@ def test_export_to_pinned_and_pageable(oracle, ctx):
         assert np.array_equal(bi, A.bi) and np.array_equal(bj, A.bj)
         assert np.array_equal(v.numpy(), A.vals)
     s.close()
+
+
+@pytest.mark.parametrize("case", ["empty_a", "empty_b", "empty_all", "disjoint_k", "zero_blocks",
+                                  "single_1x1", "eps_filters_all"])
+def test_edge_cases(oracle, ctx, case):
+    """Empty and degenerate inputs: C_out = C_in (or empty) exactly where no
+    product executes; explicit zero blocks still create C blocks (the
+    reference's pattern semantics); everything filtered by eps."""
+    from oracle.oracle import Blocks
+    from paper_1910_13555_b200.store import multiply_local
+    rs = np.array([5, 13, 23], np.int32)
+    ks = np.array([7, 13, 4, 23], np.int32)
+    ns = np.array([23, 5], np.int32)
+    A = oracle.random_matrix(1, rs, ks, 0.6)
+    B = oracle.random_matrix(2, ks, ns, 0.6)
+    Cin = oracle.random_matrix(3, rs, ns, 0.5)
+    eps = 0.0
+    if case == "empty_a":
+        A = Blocks.empty(rs, ks)
+    elif case == "empty_b":
+        B = Blocks.empty(ks, ns)
+    elif case == "empty_all":
+        A, B, Cin = Blocks.empty(rs, ks), Blocks.empty(ks, ns), Blocks.empty(rs, ns)
+    elif case == "disjoint_k":   # A only in k-columns {0, 1}, B only in k-rows {2, 3}
+        A = oracle.random_matrix(4, rs, ks, 1.0)
+        keep = A.bj < 2
+        A = _subset(A, keep)
+        B = oracle.random_matrix(5, ks, ns, 1.0)
+        B = _subset(B, B.bi >= 2)
+    elif case == "zero_blocks":  # explicit all-zero blocks are stored and multiplied
+        A = Blocks(A.rsz, A.csz, A.bi, A.bj, np.zeros_like(A.vals))
+    elif case == "single_1x1":
+        one = np.array([1], np.int32)
+        A = Blocks(one, one, np.array([0]), np.array([0]), np.array([3.0]))
+        B = Blocks(one, one, np.array([0]), np.array([0]), np.array([-2.0]))
+        Cin = Blocks(one, one, np.array([0]), np.array([0]), np.array([1.5]))
+    elif case == "eps_filters_all":
+        eps = 1e30
+    want, nprod, _ = oracle.multiply(A, B, Cin, eps)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    st = multiply_local(ctx, a, b, c, eps)
+    assert st["products"] == nprod
+    got = from_store(c)
+    assert_parity(got, want)
+    if case == "single_1x1":
+        assert got.vals.tolist() == [1.5 + 3.0 * -2.0]
+
+
+def _subset(m, keep):
+    from oracle.oracle import Blocks
+    off = m.offsets()
+    vals = np.concatenate([m.vals[off[t]:off[t + 1]] for t in np.nonzero(keep)[0]]) \
+        if keep.any() else np.zeros(0)
+    return Blocks(m.rsz, m.csz, m.bi[keep], m.bj[keep], vals)
+
+
+def test_invalid_arguments(oracle, ctx):
+    """Errors map to the reference's exception classes (errors.hpp:14-53)."""
+    from paper_1910_13555_b200 import InvalidArgument
+    from paper_1910_13555_b200.store import multiply_local
+    A = oracle.random_matrix(1, [5, 6], [7], 1.0)
+    B = oracle.random_matrix(2, [8], [3], 1.0)      # inner blockings differ
+    C = oracle.random_matrix(3, [5, 6], [3], 0.0)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, C)
+    with pytest.raises(InvalidArgument, match="inner blockings"):
+        multiply_local(ctx, a, b, c)
+    with pytest.raises(InvalidArgument, match="alias"):
+        multiply_local(ctx, a, to_store(ctx, oracle.random_matrix(4, [7], [7], 1.0)), a)
+    with pytest.raises(InvalidArgument):
+        a.put_blocks([5], [0], np.zeros(35))                 # block row out of range
