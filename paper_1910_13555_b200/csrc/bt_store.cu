@@ -236,11 +236,18 @@ __global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __
   const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (b >= nblk) return;
-  // row of entry b: binary search in row_ptr
-  int64_t lo = 0, hi = nbr;
+  // row of entry b (last r with row_ptr[r] <= b): 32-way search, one probe
+  // per lane per step, so ~log32(nbr) dependent loads instead of log2(nbr)
+  int64_t lo = 0, hi = nbr;  // row_ptr[lo] <= b < row_ptr[hi]
   while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (row_ptr[mid] <= b) lo = mid; else hi = mid;
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t probe = lo + static_cast<int64_t>(lane) * step;
+    const bool le = probe < hi && row_ptr[probe] <= b;
+    const unsigned ok = __ballot_sync(0xffffffffu, le);
+    const int last = 31 - __clz(ok);  // probe 0 (= lo) always qualifies
+    const int64_t nlo = lo + static_cast<int64_t>(last) * step;
+    hi = min(hi, nlo + step);
+    lo = nlo;
   }
   const int m = rsz[lo], n = csz[col[b]], ntc = tiles8(n);
   const double* p = vals + off[b];
