@@ -297,7 +297,6 @@ def main():
             ms_numeric.append(st["ms_numeric"])
             stats.append(st)
         torch.cuda.synchronize()
-    gc.enable()
     if world > 1:
         dist.barrier()
     kernels = ctx.kernel_count - k_before
@@ -324,6 +323,7 @@ def main():
 
     # ---- e2e through the public API with host buffers (rank-local)
     e2e_times = []
+    e2e_split = []   # debug: (put, multiply, export) ms per step, N > 1
     cout = torch.empty(NB * NB * bsize, dtype=torch.float64).pin_memory()
     h2d = av.nbytes + bv.nbytes + 16 * (len(abi) + len(bbi))
     d2h = 0
@@ -351,16 +351,22 @@ def main():
             c.local(rank).clear()
             a.local(rank).put_blocks(abi + NB * rank, abj, av_pin)
             b.local(rank).put_blocks(bbi, bbj, bv_pin)
+            t1 = time.perf_counter()
             dd.multiply_virtual_case2(comm, a, b, c, world, gather=True)
+            t2 = time.perf_counter()
             ci, cj, _ = c.local(rank).export(cout)
             ctx.sync()
             dt = time.perf_counter() - t0
+            if os.environ.get("BT_BENCH_DEBUG"):
+                e2e_split.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2),
+                                  round(1e3 * (dt - (t2 - t0)), 2)))
             d2h = 8 * int(c.local(rank).info()[1]) + 16 * len(ci)
         if s >= args.warmup:
             e2e_times.append(dt)
     if os.environ.get("BT_BENCH_DEBUG"):
-        print(f"[rank {rank}] e2e_ms {np.round(np.array(e2e_times) * 1e3, 2).tolist()}",
-              file=sys.stderr, flush=True)
+        print(f"[rank {rank}] e2e_ms {np.round(np.array(e2e_times) * 1e3, 2).tolist()} "
+              f"split(put,mult,export) {e2e_split}", file=sys.stderr, flush=True)
+    gc.enable()
     e2e_s = float(np.mean(e2e_times))
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64)

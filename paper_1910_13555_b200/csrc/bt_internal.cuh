@@ -157,6 +157,9 @@ struct Mat {
   DBuf<double> vals;
   cudaStream_t stream() const { return ctx->stream; }
   void init_empty();  // empty pattern (row_ptr all zero)
+  // empty pattern, keeping col/off/vals allocated as capacity for the next
+  // multiply into this store (bt_mat_clear)
+  void clear_keep_capacity();
 };
 
 __host__ __device__ inline int64_t pad2(int64_t x) { return (x + 1) & ~int64_t(1); }

@@ -926,8 +926,20 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
                BT_ERR_INVALID_ARGUMENT, "multiply: operand slab exceeds 2^31 tiles");
 
     // ---- pass 2: C_out pattern, product stacks (descriptors)
-    DBuf<int32_t> out_col(std::max<int64_t>(nout, 1), st);
-    DBuf<int64_t> out_off(std::max<int64_t>(nout, 1), st);
+    // An empty C (no C_in blocks: nothing reads its col/off/vals) hands its
+    // buffers over as the outputs when they are large enough -- a repeated
+    // clear + multiply then allocates nothing
+    const bool reuse_c = Cm.nblk == 0;
+    DBuf<int32_t> out_col;
+    DBuf<int64_t> out_off;
+    if (reuse_c && Cm.col.n >= static_cast<size_t>(std::max<int64_t>(nout, 1)) &&
+        Cm.off.n >= static_cast<size_t>(std::max<int64_t>(nout, 1))) {
+      out_col = std::move(Cm.col);
+      out_off = std::move(Cm.off);
+    } else {
+      out_col.alloc(std::max<int64_t>(nout, 1), st);
+      out_off.alloc(std::max<int64_t>(nout, 1), st);
+    }
     int32_t* out_row = x.ws<int32_t>(6, nout);
     int32_t* out_np = x.ws<int32_t>(7, nout);
     int64_t* cin_map = x.ws<int64_t>(8, nout);
@@ -962,7 +974,12 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
 
     tr.mark("pass2 enqueued");
     // ---- numeric phase: one kernel per tile class, classes run concurrently
-    DBuf<double> new_vals(std::max<int64_t>(nvals, 64), st);
+    DBuf<double> new_vals;
+    if (reuse_c && Cm.vals.n >= static_cast<size_t>(std::max<int64_t>(nvals, 64)))
+      new_vals = std::move(Cm.vals);
+    else
+      new_vals.alloc(std::max<int64_t>(nvals, 64), st);
+    tr.mark("C slab");
     if (nout > 0) {
       NumArgs g{};
       g.items = items;

@@ -123,6 +123,14 @@ void upload_sizes(Mat& m) {
                                           [&](int32_t s) { return s == m.h_csz[0]; });
 }
 
+void Mat::clear_keep_capacity() {
+  nblk = 0;
+  nelems = 0;
+  nvals = 0;
+  if (row_ptr.n < static_cast<size_t>(nbr + 1)) row_ptr.alloc(nbr + 1, stream());
+  BT_CUDA(cudaMemsetAsync(row_ptr.p, 0, sizeof(int32_t) * (nbr + 1), stream()));
+}
+
 void Mat::init_empty() {
   nblk = 0;
   nelems = 0;
@@ -521,7 +529,7 @@ int bt_mat_destroy(bt_mat* m) {
 int bt_mat_clear(bt_mat* m) {
   return guard([&] {
     check_mat(m);
-    m->impl.init_empty();
+    m->impl.clear_keep_capacity();
   });
 }
 
