@@ -123,9 +123,98 @@ struct Contribution {
   bool transpose;
 };
 
+// Device side of merge_into: one thread per contributed entry writes its
+// destination key, its position in contribution order, the source block pointer
+// and the transposed flag at [base, base + n).
+__global__ void k_merge_keys(const int32_t* __restrict__ rp, int64_t nbr,
+                             const int32_t* __restrict__ col, const int64_t* __restrict__ off,
+                             const double* vals, const int64_t* __restrict__ sel, int64_t n,
+                             int tr, int64_t nbc, int64_t base, int64_t* __restrict__ key,
+                             int64_t* __restrict__ pos, const double** __restrict__ src,
+                             uint8_t* __restrict__ trf) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int64_t e = sel ? sel[q] : q;
+  int64_t lo = 0, hi = nbr;  // row = last i with rp[i] <= e
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rp[mid] <= e) lo = mid; else hi = mid;
+  }
+  const int64_t i = lo, j = col[e];
+  key[base + q] = tr ? j * nbc + i : i * nbc + j;
+  pos[base + q] = base + q;
+  src[base + q] = vals + off[e];
+  trf[base + q] = static_cast<uint8_t>(tr);
+}
+
+// Over the key-sorted contributions: segment heads, their T8 value sizes and
+// element counts (zero elsewhere), and the sources/flags in sorted order.
+__global__ void k_merge_heads(const int64_t* __restrict__ skey, const int64_t* __restrict__ spos,
+                              int64_t total, int64_t nbc, const int32_t* __restrict__ rsz,
+                              const int32_t* __restrict__ csz, const double* const* __restrict__ src,
+                              const uint8_t* __restrict__ trf, int32_t* __restrict__ head,
+                              int64_t* __restrict__ vsz, int64_t* __restrict__ esz,
+                              const double** __restrict__ ssrc, uint8_t* __restrict__ strf) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > total) return;
+  if (t == total) {  // trailing zero: the exclusive scans' last element is the total
+    head[t] = 0;
+    vsz[t] = 0;
+    esz[t] = 0;
+    return;
+  }
+  const int64_t k = skey[t];
+  const bool h = t == 0 || skey[t - 1] != k;
+  const int m = rsz[k / nbc], n = csz[k % nbc];
+  head[t] = h ? 1 : 0;
+  vsz[t] = h ? t8_size(m, n) : 0;
+  esz[t] = h ? int64_t(m) * n : 0;
+  ssrc[t] = src[spos[t]];
+  strf[t] = trf[spos[t]];
+}
+
+// Compacts the heads into the output index (col, off, segment start, key) and
+// writes the totals (blocks, values, elements) for the host.
+__global__ void k_merge_compact(const int64_t* __restrict__ skey, int64_t total,
+                                const int32_t* __restrict__ head, const int32_t* __restrict__ hscan,
+                                const int64_t* __restrict__ vscan, const int64_t* __restrict__ escan,
+                                int64_t nbc, int32_t* __restrict__ ocol, int64_t* __restrict__ ooff,
+                                int64_t* __restrict__ oseg, int64_t* __restrict__ okey,
+                                int64_t* __restrict__ totals) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t == 0) {
+    totals[0] = hscan[total];
+    totals[1] = vscan[total];
+    totals[2] = escan[total];
+    oseg[hscan[total]] = total;
+  }
+  if (t >= total || !head[t]) return;
+  const int64_t u = hscan[t];
+  ocol[u] = static_cast<int32_t>(skey[t] % nbc);
+  ooff[u] = vscan[t];
+  oseg[u] = t;
+  okey[u] = skey[t];
+}
+
+// row_ptr[i] = first output block with key >= i * nbc
+__global__ void k_merge_rowptr(const int64_t* __restrict__ okey, const int64_t* __restrict__ totals,
+                               int64_t nbr, int64_t nbc, int32_t* __restrict__ rp) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > nbr) return;
+  const int64_t target = i * nbc;
+  int64_t lo = 0, hi = totals[0];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (okey[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  rp[i] = static_cast<int32_t>(lo);
+}
+
 // Builds dst := (accumulate ? dst : {}) merged with the contributions, in order.
 // Blocks present in several contributions are summed in contribution order
 // (accumulate) or the last one wins (LocalStore::insert, matrix.hpp:167-189).
+// All index work is on the device (stable radix sort by destination key); the
+// host reads back the three totals once, to size the value buffer.
 void merge_into(Mat& dst, const std::vector<Contribution>& parts, bool accumulate) {
   Ctx& x = *dst.ctx;
   cudaStream_t st = x.stream;
@@ -136,100 +225,67 @@ void merge_into(Mat& dst, const std::vector<Contribution>& parts, bool accumulat
     dst.init_empty();
     return;
   }
-  // gather (key, src pointer, transposed) for every contribution
-  std::vector<int64_t> h_keys;
-  std::vector<const double*> h_src;
-  std::vector<uint8_t> h_tr;
-  h_keys.reserve(total);
-  h_src.reserve(total);
-  h_tr.reserve(total);
+  DBuf<int64_t> key(total, st), skey(total, st), pos(total, st), spos(total, st);
+  DBuf<const double*> src(total, st), ssrc(total, st);
+  DBuf<uint8_t> trf(total, st), strf(total, st);
+  int64_t base = 0;
   auto add_part = [&](const Mat& m, const int64_t* sel, int64_t n, bool tr) {
     if (n == 0) return;
-    std::vector<int32_t> rp(m.nbr + 1), col(m.nblk);
-    std::vector<int64_t> off(m.nblk);
-    BT_CUDA(cudaMemcpyAsync(rp.data(), m.row_ptr.p, 4 * (m.nbr + 1), cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(col.data(), m.col.p, 4 * m.nblk, cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(off.data(), m.off.p, 8 * m.nblk, cudaMemcpyDeviceToHost, st));
-    std::vector<int64_t> hsel;
-    if (sel) {
-      hsel.resize(n);
-      BT_CUDA(cudaMemcpyAsync(hsel.data(), sel, 8 * n, cudaMemcpyDeviceToHost, st));
-    }
-    BT_CUDA(cudaStreamSynchronize(st));
-    std::vector<int32_t> row(m.nblk);
-    for (int64_t i = 0; i < m.nbr; ++i)
-      for (int32_t e = rp[i]; e < rp[i + 1]; ++e) row[e] = static_cast<int32_t>(i);
-    for (int64_t q = 0; q < n; ++q) {
-      const int64_t e = sel ? hsel[q] : q;
-      const int64_t i = row[e], j = col[e];
-      h_keys.push_back(tr ? j * nbc + i : i * nbc + j);
-      h_src.push_back(m.vals.p + off[e]);
-      h_tr.push_back(tr ? 1 : 0);
-    }
+    k_merge_keys<<<nb(n, 256), 256, 0, st>>>(m.row_ptr.p, m.nbr, m.col.p, m.off.p, m.vals.p, sel,
+                                             n, tr ? 1 : 0, nbc, base, key.p, pos.p, src.p, trf.p);
+    check_launch("merge_keys");
+    count_launch(&x);
+    base += n;
   };
   if (accumulate) add_part(dst, nullptr, dst.nblk, false);
   for (const auto& p : parts) add_part(*p.src, p.sel, p.n, p.transpose);
-  // stable order by key (host: index-sized work, values stay on the device)
-  std::vector<int64_t> perm(h_keys.size());
-  std::iota(perm.begin(), perm.end(), 0);
-  std::stable_sort(perm.begin(), perm.end(),
-                   [&](int64_t a, int64_t b) { return h_keys[a] < h_keys[b]; });
-  std::vector<int64_t> skey(perm.size()), seg;
-  std::vector<const double*> ssrc(perm.size());
-  std::vector<uint8_t> str(perm.size());
-  for (size_t t = 0; t < perm.size(); ++t) {
-    skey[t] = h_keys[perm[t]];
-    ssrc[t] = h_src[perm[t]];
-    str[t] = h_tr[perm[t]];
-  }
-  std::vector<int32_t> row_ptr(dst.nbr + 1, 0), col;
-  std::vector<int64_t> off;
-  int64_t nv = 0, ne = 0;
-  for (size_t t = 0; t < skey.size(); ++t) {
-    if (t > 0 && skey[t] == skey[t - 1]) continue;
-    seg.push_back(static_cast<int64_t>(t));
-    const int64_t i = skey[t] / nbc, j = skey[t] % nbc;
-    col.push_back(static_cast<int32_t>(j));
-    off.push_back(nv);
-    row_ptr[i + 1]++;
-    nv += t8_size(dst.h_rsz[i], dst.h_csz[j]);
-    ne += int64_t(dst.h_rsz[i]) * dst.h_csz[j];
-  }
-  seg.push_back(static_cast<int64_t>(skey.size()));
-  for (int64_t i = 0; i < dst.nbr; ++i) row_ptr[i + 1] += row_ptr[i];
-  const int64_t nout = static_cast<int64_t>(col.size());
-  DBuf<int64_t> d_key(skey.size(), st), d_seg(seg.size(), st), d_off(nout, st);
-  DBuf<const double*> d_src(ssrc.size(), st);
-  DBuf<uint8_t> d_tr(str.size(), st);
-  BT_CUDA(cudaMemcpyAsync(d_key.p, skey.data(), 8 * skey.size(), cudaMemcpyHostToDevice, st));
-  BT_CUDA(cudaMemcpyAsync(d_seg.p, seg.data(), 8 * seg.size(), cudaMemcpyHostToDevice, st));
-  BT_CUDA(cudaMemcpyAsync(d_off.p, off.data(), 8 * nout, cudaMemcpyHostToDevice, st));
-  BT_CUDA(cudaMemcpyAsync(d_src.p, ssrc.data(), sizeof(void*) * ssrc.size(),
-                          cudaMemcpyHostToDevice, st));
-  BT_CUDA(cudaMemcpyAsync(d_tr.p, str.data(), str.size(), cudaMemcpyHostToDevice, st));
+  // stable (radix) sort by key keeps contribution order within a block
+  const uint64_t kmax = static_cast<uint64_t>(std::max<int64_t>(dst.nbr * nbc, 1));
+  const int end_bit = std::max(1, 64 - __builtin_clzll(kmax));
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, skey.p, pos.p, spos.p, total, 0, end_bit,
+                                  st);
+  void* tmp = x.ensure_scratch(bytes);
+  cub::DeviceRadixSort::SortPairs(tmp, bytes, key.p, skey.p, pos.p, spos.p, total, 0, end_bit, st);
+  count_launch(&x, 4);
+  DBuf<int32_t> head(total + 1, st), hscan(total + 1, st);
+  DBuf<int64_t> vsz(total + 1, st), vscan(total + 1, st), esz(total + 1, st), escan(total + 1, st);
+  k_merge_heads<<<nb(total + 1, 256), 256, 0, st>>>(skey.p, spos.p, total, nbc, dst.rsz.p,
+                                                    dst.csz.p, src.p, trf.p, head.p, vsz.p, esz.p,
+                                                    ssrc.p, strf.p);
+  check_launch("merge_heads");
+  count_launch(&x);
+  dscan(x, head.p, hscan.p, total + 1);
+  dscan(x, vsz.p, vscan.p, total + 1);
+  dscan(x, esz.p, escan.p, total + 1);
+  // outputs sized for the worst case (every contribution its own block)
+  DBuf<int32_t> cl(total, st), rp(dst.nbr + 1, st);
+  DBuf<int64_t> of(total, st), seg(total + 1, st), okey(total, st), tot(3, st);
+  k_merge_compact<<<nb(total, 256), 256, 0, st>>>(skey.p, total, head.p, hscan.p, vscan.p,
+                                                  escan.p, nbc, cl.p, of.p, seg.p, okey.p, tot.p);
+  check_launch("merge_compact");
+  k_merge_rowptr<<<nb(dst.nbr + 1, 256), 256, 0, st>>>(okey.p, tot.p, dst.nbr, nbc, rp.p);
+  check_launch("merge_rowptr");
+  count_launch(&x, 2);
+  int64_t h_tot[3];
+  BT_CUDA(cudaMemcpyAsync(h_tot, tot.p, sizeof(h_tot), cudaMemcpyDeviceToHost, st));
+  BT_CUDA(cudaStreamSynchronize(st));
+  const int64_t nout = h_tot[0], nv = h_tot[1], ne = h_tot[2];
   DBuf<double> vals(std::max<int64_t>(nv, 64), st);
   BT_CUDA(cudaMemsetAsync(vals.p, 0, 8 * std::max<int64_t>(nv, 64), st));  // T8 padding = 0
-  k_merge_vals<<<static_cast<unsigned>(nout), 128, 0, st>>>(d_key.p, d_seg.p, nout, d_src.p,
-                                                            d_tr.p, nbc, dst.rsz.p, dst.csz.p,
-                                                            d_off.p, accumulate ? 1 : 0, vals.p);
+  k_merge_vals<<<static_cast<unsigned>(nout), 128, 0, st>>>(skey.p, seg.p, nout, ssrc.p, strf.p,
+                                                            nbc, dst.rsz.p, dst.csz.p, of.p,
+                                                            accumulate ? 1 : 0, vals.p);
   check_launch("merge_vals");
   count_launch(&x);
   BT_CUDA(cudaStreamSynchronize(st));  // sources may be released by the caller
   dst.vals = std::move(vals);
-  DBuf<int32_t> rp(dst.nbr + 1, st), cl(std::max<int64_t>(nout, 1), st);
-  DBuf<int64_t> of(std::max<int64_t>(nout, 1), st);
-  BT_CUDA(cudaMemcpyAsync(rp.p, row_ptr.data(), 4 * (dst.nbr + 1), cudaMemcpyHostToDevice, st));
-  if (nout) {
-    BT_CUDA(cudaMemcpyAsync(cl.p, col.data(), 4 * nout, cudaMemcpyHostToDevice, st));
-    BT_CUDA(cudaMemcpyAsync(of.p, off.data(), 8 * nout, cudaMemcpyHostToDevice, st));
-  }
   dst.row_ptr = std::move(rp);
   dst.col = std::move(cl);
   dst.off = std::move(of);
   dst.nblk = nout;
   dst.nvals = nv;
   dst.nelems = ne;
-  BT_CUDA(cudaStreamSynchronize(st));
 }
 
 // entry indices (device) of the entries of `m` whose owner (under the layout,
@@ -538,6 +594,7 @@ void redistribute(const DMat& src, DMat& dst, bool transpose, bool accumulate,
     BT_REQUIRE(src.rsz == dst.csz && src.csz == dst.rsz, BT_ERR_INVALID_ARGUMENT,
                "redistribute: transposed target blockings do not match");
   g.set_phase(phase);
+  Trace tr("redistribute");
   DBuf<int32_t> rdist(std::max<size_t>(dst.rdist.size(), 1), st),
       cdist(std::max<size_t>(dst.cdist.size(), 1), st);
   BT_CUDA(cudaMemcpyAsync(rdist.p, dst.rdist.data(), 4 * dst.rdist.size(), cudaMemcpyHostToDevice, st));
@@ -562,6 +619,7 @@ void redistribute(const DMat& src, DMat& dst, bool transpose, bool accumulate,
       out[lr].push_back(std::move(bucket));
     }
   }
+  tr.mark("buckets");
   // exchange: step t, rank r sends to (r+t)%P and receives from (r-t)%P
   // (exchange_blocks, matrix.hpp:545-560); deliveries merged in that order
   std::vector<std::vector<std::unique_ptr<bt_mat>>> in(g.nlocal);
@@ -577,6 +635,7 @@ void redistribute(const DMat& src, DMat& dst, bool transpose, bool accumulate,
       recvs.push_back(Recv{r, from, &in[lr][t]->impl});
     }
   exchange(g, sends, recvs);
+  tr.mark("exchange");
   for (int lr = 0; lr < g.nlocal; ++lr) {
     std::vector<Contribution> parts;
     for (int t = 0; t < P; ++t) {
@@ -587,6 +646,7 @@ void redistribute(const DMat& src, DMat& dst, bool transpose, bool accumulate,
     if (!accumulate) d.init_empty();
     merge_into(d, parts, accumulate);
   }
+  tr.mark("merge");
 }
 
 }  // namespace bt
