@@ -305,6 +305,127 @@ int64_t select_owned(Mat& m, const int32_t* d_owner, int target, DBuf<int64_t>& 
   return n;
 }
 
+// ---- one-pass split of a store by owner (non-transposed redistribute)
+// Per entry: its row, the sort key (owner) and identity payload; per owner: the
+// entry, value and element totals.
+__global__ void k_split_hist(const int32_t* __restrict__ rp, int64_t nbr,
+                             const int32_t* __restrict__ col, const int32_t* __restrict__ owner,
+                             const int32_t* __restrict__ rsz, const int32_t* __restrict__ csz,
+                             int P, int32_t* __restrict__ row_of, int32_t* __restrict__ ident,
+                             unsigned long long* __restrict__ hist) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nbr) return;
+  for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
+    const int m = rsz[i], n = csz[col[e]], d = owner[e];
+    row_of[e] = static_cast<int32_t>(i);
+    ident[e] = e;
+    atomicAdd(&hist[d], 1ull);
+    atomicAdd(&hist[P + d], static_cast<unsigned long long>(t8_size(m, n)));
+    atomicAdd(&hist[2 * P + d], static_cast<unsigned long long>(m) * n);
+  }
+}
+
+// T8 value sizes of the owner-sorted entries (plus a trailing zero)
+__global__ void k_split_vsz(const int32_t* __restrict__ ord, int64_t n,
+                            const int32_t* __restrict__ row_of, const int32_t* __restrict__ col,
+                            const int32_t* __restrict__ rsz, const int32_t* __restrict__ csz,
+                            int64_t* __restrict__ vsz) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > n) return;
+  if (t == n) { vsz[t] = 0; return; }
+  const int32_t e = ord[t];
+  vsz[t] = t8_size(rsz[row_of[e]], csz[col[e]]);
+}
+
+// One bucket: entries ord[t0, t0 + n) (key order) -> col/off, values copied
+// warp per block.
+__global__ void k_split_fill(const int32_t* __restrict__ ord, int64_t t0, int64_t n,
+                             const int32_t* __restrict__ col, const int64_t* __restrict__ off,
+                             const double* __restrict__ vals, const int64_t* __restrict__ vscan,
+                             int32_t* __restrict__ bcol, int64_t* __restrict__ boff,
+                             double* __restrict__ bvals) {
+  const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (q >= n) return;
+  const int32_t e = ord[t0 + q];
+  const int64_t o = vscan[t0 + q] - vscan[t0], len = vscan[t0 + q + 1] - vscan[t0 + q];
+  if (lane == 0) {
+    bcol[q] = col[e];
+    boff[q] = o;
+  }
+  const double2* s2 = reinterpret_cast<const double2*>(vals + off[e]);
+  double2* d2 = reinterpret_cast<double2*>(bvals + o);
+  for (int64_t k = lane; k < len / 2; k += 32) d2[k] = s2[k];
+}
+
+// bucket row_ptr[i] = first bucket entry whose row is >= i
+__global__ void k_split_rowptr(const int32_t* __restrict__ ord, int64_t t0, int64_t n,
+                               const int32_t* __restrict__ row_of, int64_t nbr,
+                               int32_t* __restrict__ rp) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > nbr) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (row_of[ord[t0 + mid]] < i) lo = mid + 1; else hi = mid;
+  }
+  rp[i] = static_cast<int32_t>(lo);
+}
+
+// Splits `s` into P stores by the per-entry owner: one stable radix sort by
+// owner and a single readback of the per-owner totals (vs. a select + merge
+// per destination).
+void split_by_owner(Ctx& x, const Mat& s, const int32_t* d_owner, int P,
+                    std::vector<std::unique_ptr<bt_mat>>& out) {
+  cudaStream_t st = x.stream;
+  const int64_t n = s.nblk;
+  DBuf<int32_t> row_of(n, st), ident(n, st), okey(n, st), ord(n, st);
+  DBuf<unsigned long long> hist(3 * P, st);
+  BT_CUDA(cudaMemsetAsync(hist.p, 0, 8 * 3 * P, st));
+  k_split_hist<<<nb(s.nbr, 128), 128, 0, st>>>(s.row_ptr.p, s.nbr, s.col.p, d_owner, s.rsz.p,
+                                               s.csz.p, P, row_of.p, ident.p, hist.p);
+  check_launch("split_hist");
+  const int end_bit = std::max(1, 32 - __builtin_clz(static_cast<unsigned>(std::max(P - 1, 1))));
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, d_owner, okey.p, ident.p, ord.p, n, 0, end_bit,
+                                  st);
+  void* tmp = x.ensure_scratch(bytes);
+  cub::DeviceRadixSort::SortPairs(tmp, bytes, d_owner, okey.p, ident.p, ord.p, n, 0, end_bit, st);
+  DBuf<int64_t> vsz(n + 1, st), vscan(n + 1, st);
+  k_split_vsz<<<nb(n + 1, 256), 256, 0, st>>>(ord.p, n, row_of.p, s.col.p, s.rsz.p, s.csz.p,
+                                              vsz.p);
+  check_launch("split_vsz");
+  dscan(x, vsz.p, vscan.p, n + 1);
+  count_launch(&x, 6);
+  std::vector<unsigned long long> h(3 * P);
+  BT_CUDA(cudaMemcpyAsync(h.data(), hist.p, 8 * 3 * P, cudaMemcpyDeviceToHost, st));
+  BT_CUDA(cudaStreamSynchronize(st));
+  int64_t t0 = 0;
+  for (int d = 0; d < P; ++d) {
+    const int64_t nd = static_cast<int64_t>(h[d]);
+    Mat& b = out[d]->impl;
+    if (nd) {
+      b.row_ptr.alloc(b.nbr + 1, st);
+      b.col.alloc(nd, st);
+      b.off.alloc(nd, st);
+      const int64_t nv = static_cast<int64_t>(h[P + d]);
+      b.vals.alloc(std::max<int64_t>(nv, 64), st);
+      k_split_fill<<<nb(nd * 32, 256), 256, 0, st>>>(ord.p, t0, nd, s.col.p, s.off.p, s.vals.p,
+                                                     vscan.p, b.col.p, b.off.p, b.vals.p);
+      check_launch("split_fill");
+      k_split_rowptr<<<nb(b.nbr + 1, 256), 256, 0, st>>>(ord.p, t0, nd, row_of.p, b.nbr,
+                                                         b.row_ptr.p);
+      check_launch("split_rowptr");
+      count_launch(&x, 2);
+      b.nblk = nd;
+      b.nvals = nv;
+      b.nelems = static_cast<int64_t>(h[2 * P + d]);
+    }
+    t0 += nd;
+  }
+  BT_CUDA(cudaStreamSynchronize(st));  // the temporaries above are released on return
+}
+
 // ================================================================= group
 struct Counters {
   int64_t v[4] = {0, 0, 0, 0};  // elements sent, received, meta sent, received
@@ -610,6 +731,11 @@ void redistribute(const DMat& src, DMat& dst, bool transpose, bool accumulate,
       k_owner<<<nb(s.nbr, 128), 128, 0, st>>>(s.row_ptr.p, s.col.p, s.nbr, rdist.p, cdist.p,
                                               dst.gc, transpose ? 1 : 0, owner.p);
       count_launch(&x);
+    }
+    if (!transpose && s.nblk) {
+      for (int d = 0; d < P; ++d) out[lr].push_back(new_store(g.ctx, dst.rsz, dst.csz));
+      split_by_owner(x, s, owner.p, P, out[lr]);
+      continue;
     }
     for (int d = 0; d < P; ++d) {
       auto bucket = new_store(g.ctx, dst.rsz, dst.csz);
