@@ -708,6 +708,24 @@ KernelFn dmma_kernel(int cls, int stages) {
   return stages >= 2 ? dmma_kernel_s<2>(cls) : dmma_kernel_s<1>(cls);
 }
 
+// the K-panels-in-one-launch variant of a class
+template <int S>
+KernelFn dmma_panel_kernel_s(int cls) {
+  static const KernelFn table[16] = {
+      k_smm_dmma<1, 1, kWarps, S, false, true>, k_smm_dmma<1, 2, kWarps, S, false, true>,
+      k_smm_dmma<1, 3, kWarps, S, false, true>, k_smm_dmma<1, 4, kWarps, S, false, true>,
+      k_smm_dmma<2, 1, kWarps, S, false, true>, k_smm_dmma<2, 2, kWarps, S, false, true>,
+      k_smm_dmma<2, 3, kWarps, S, false, true>, k_smm_dmma<2, 4, kWarps, S, false, true>,
+      k_smm_dmma<3, 1, kWarps, S, false, true>, k_smm_dmma<3, 2, kWarps, S, false, true>,
+      k_smm_dmma<3, 3, kWarps, S, false, true>, k_smm_dmma<3, 4, kWarps, S, false, true>,
+      k_smm_dmma<4, 1, kWarps, S, false, true>, k_smm_dmma<4, 2, kWarps, S, false, true>,
+      k_smm_dmma<4, 3, kWarps, S, false, true>, k_smm_dmma<4, 4, kWarps, S, false, true>};
+  return table[cls];
+}
+KernelFn dmma_panel_kernel(int cls, int stages) {
+  return stages >= 2 ? dmma_panel_kernel_s<2>(cls) : dmma_panel_kernel_s<1>(cls);
+}
+
 // Dynamic shared-memory opt-in per (device, kernel): the largest size set so
 // far, raised when a launch needs more.  Thread-safe (one context per host
 // thread may drive its own device).
@@ -982,6 +1000,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     tr.mark("C slab");
     if (nout > 0) {
       NumArgs g{};
+      g.npanels = 1;
       g.items = items;
       g.desc = desc;
       g.at = A.vals.p;
@@ -1026,7 +1045,42 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       if (wait_numeric) BT_CUDA(cudaStreamWaitEvent(st, wait_numeric, 0));
       if (numeric_start) BT_CUDA(cudaEventRecord(numeric_start, st));
       if (x.timing) BT_CUDA(cudaEventRecord(x.ev[1], st));
-      for (int panel = 0; panel < npanels; ++panel) {
+      // panels of a single DMMA class run as ONE launch (per-tile flags order
+      // the in-place accumulation; one tail instead of one per panel)
+      int only = -1, present = 0;
+      for (int q = 0; q < NCLASS; ++q)
+        if (ibound[q + 1] > ibound[q]) {
+          only = q;
+          ++present;
+        }
+      const bool fused = npanels > 1 && present == 1 && only != GENERIC &&
+                         env_int("BT_PANEL_FUSE", 1) != 0;
+      if (fused) {
+        const int q = only;
+        const int64_t lo = ibound[q], hi = ibound[q + 1];
+        const int ktmax = std::max(1, tiles8(kmax));
+        const Plan P = plan_dmma(q, ktmax);
+        g.stages = P.stages;
+        g.stage_doubles = P.stage_doubles;
+        g.a_region = P.a_region;
+        g.items = pitems;
+        g.item_lo = lo;
+        g.nitems = hi - lo;
+        g.npanels = npanels;
+        g.panel_stride = nitems;
+        g.tile_flag = x.ws<int>(21, nitems) + lo;
+        BT_CUDA(cudaMemsetAsync(x.ws<int>(21, nitems), 0, 4 * nitems, st));
+        g.counter = counters + q;
+        KernelFn fn = dmma_panel_kernel(q, P.stages);
+        const int per_sm = dmma_occupancy(fn, P.smem);
+        BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
+        const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,
+                                               (hi - lo + kWarps - 1) / kWarps);
+        fn<<<static_cast<unsigned>(grid), kWarps * 32, P.smem, st>>>(g);
+        check_launch("smm_dmma_panels");
+        count_launch(&x);
+      }
+      for (int panel = 0; panel < (fused ? 0 : npanels); ++panel) {
       g.items = pitems + static_cast<int64_t>(panel) * nitems;
       if (panel > 0) {  // later panels accumulate into C_out in place
         g.cin = g.cout;

@@ -51,7 +51,23 @@ struct NumArgs {
   int stages;
   int stage_doubles;  // per-stage shared memory in doubles
   int a_region;       // doubles of the A part of a stage
+  // K panels in one launch (npanels > 1): ticket t is item t % nitems of panel
+  // t / nitems (items of panel p at items + p * panel_stride); panels p > 0
+  // accumulate into C_out in place once tile_flag[item] says panel p - 1 of
+  // the same tile has stored its C
+  int npanels;
+  int64_t panel_stride;
+  int* tile_flag;
 };
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ int64_t item_p0(const Item& it) {
   return it.p0r8 & ((int64_t(1) << 48) - 1);
@@ -83,7 +99,10 @@ constexpr int dmma_min_blocks() {
 // is then the largest tile, each item's own tile shape comes from its rows and
 // columns, and the consumer dispatches to the matching instantiation of the
 // tile body (so small classes do not pay for the large accumulators).
-template <int TMT, int TNT, int WARPS, int S, bool MULTI = false>
+// PANELS: every K panel of a single-class multiply in one launch (NumArgs
+// npanels / panel_stride / tile_flag); a separate instantiation so the common
+// path carries none of its bookkeeping.
+template <int TMT, int TNT, int WARPS, int S, bool MULTI = false, bool PANELS = false>
 __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_smm_dmma(const NumArgs g) {
   constexpr int QN = 8;     // item slots per warp
   constexpr int CTL = 1536; // control block bytes per warp
@@ -101,10 +120,17 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
   uint64_t* bars = reinterpret_cast<uint64_t*>(ctl);
   int* stage_kc = reinterpret_cast<int*>(ctl + 64);
   Item* q_items = reinterpret_cast<Item*>(ctl + 128);
+  int64_t* q_tick = reinterpret_cast<int64_t*>(ctl + 384);  // ticket of each item slot
   Desc* dring = reinterpret_cast<Desc*>(ctl + 512);  // [2][32]
   double* stages = reinterpret_cast<double*>(smem + WARPS * CTL) +
                    static_cast<int64_t>(wid) * S * g.stage_doubles;
   const Item* items = g.items + g.item_lo;
+  const int64_t ntickets = PANELS ? g.nitems * g.npanels : g.nitems;
+  auto item_at = [&](int64_t id) -> const Item* {
+    if constexpr (!PANELS) return items + id;
+    const int64_t p = id / g.nitems;
+    return items + p * g.panel_stride + (id - p * g.nitems);
+  };
 
   // ---- prologue: tickets for items 0 and 1, their structs, ticket for item 2
   unsigned long long tk = 0;  // lane 0: ticket of the item two ahead
@@ -113,10 +139,12 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
     fence_mbar_init();
     for (int n = 0; n < 2; ++n) {
       const unsigned long long id = atomicAdd(g.counter, 1ull);
-      if (static_cast<int64_t>(id) < g.nitems) {
-        cp_async16(&q_items[n], &items[id]);
+      if (static_cast<int64_t>(id) < ntickets) {
+        const Item* src = item_at(static_cast<int64_t>(id));
+        cp_async16(&q_items[n], src);
         cp_async16(reinterpret_cast<char*>(&q_items[n]) + 16,
-                   reinterpret_cast<const char*>(&items[id]) + 16);
+                   reinterpret_cast<const char*>(src) + 16);
+        if constexpr (PANELS) q_tick[n] = static_cast<int64_t>(id);
       } else {
         q_items[n].np = -1;  // end of work
       }
@@ -202,10 +230,11 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         // ticket of item qt+3
         if (lane == 0) {
           Item* dst = &q_items[(qt + 2) % QN];
-          if (static_cast<int64_t>(tk) < g.nitems) {
-            cp_async16(dst, &items[tk]);
-            cp_async16(reinterpret_cast<char*>(dst) + 16,
-                       reinterpret_cast<const char*>(&items[tk]) + 16);
+          if (static_cast<int64_t>(tk) < ntickets) {
+            const Item* src = item_at(static_cast<int64_t>(tk));
+            cp_async16(dst, src);
+            cp_async16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
+            if constexpr (PANELS) q_tick[(qt + 2) % QN] = static_cast<int64_t>(tk);
             tk = atomicAdd(g.counter, 1ull);
           } else {
             dst->np = -1;
@@ -249,7 +278,23 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
   while (qh < qt) {
     const Item it = q_items[qh % QN];
     const int mt = (it.rows + 7) >> 3;  // 8-row tiles present in this C tile
-    if (it.np == 0 && it.cin_off == it.c_off && g.cin == g.cout) {  // in-place, no products
+    // panels in one launch: wait until the previous panel of this tile is stored
+    int panel = 0;
+    int* flag = nullptr;
+    if constexpr (PANELS) {
+      const int64_t tick = q_tick[qh % QN];
+      panel = static_cast<int>(tick / g.nitems);
+      flag = g.tile_flag + (tick - static_cast<int64_t>(panel) * g.nitems);
+      if (panel > 0) {
+        if (lane == 0)
+          while (ld_acquire_gpu(flag) < panel) __nanosleep(32);
+        __syncwarp();
+      }
+    }
+    const double* cin = panel > 0 ? g.cout : g.cin;
+    if (it.np == 0 && it.cin_off == it.c_off && cin == g.cout) {  // in-place, no products
+      if constexpr (PANELS)
+        if (lane == 0) st_release_gpu(flag, panel + 1);
       ++qh;
       top_up();
       __syncwarp();
@@ -272,8 +317,10 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
           if (tm < mt) {
 #pragma unroll
             for (int tn = 0; tn < CN; ++tn) {
-              const double2 v = *reinterpret_cast<const double2*>(
-                  g.cin + it.cin_off + ((tm * CN + tn) << 6) + lc);
+              // PANELS: L2 loads, the tile may have been stored by another SM
+              const double2* src = reinterpret_cast<const double2*>(
+                  cin + it.cin_off + ((tm * CN + tn) << 6) + lc);
+              const double2 v = PANELS ? __ldcg(src) : *src;
               acc[tm][tn][0] = v.x;
               acc[tm][tn][1] = v.y;
             }
@@ -336,6 +383,11 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
             __stcs(reinterpret_cast<double2*>(dst + ((tm * CN + tn) << 6) + lc),
                    make_double2(acc[tm][tn][0], acc[tm][tn][1]));
         }
+      if constexpr (PANELS) {  // publish: this panel of the tile is stored
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(flag, panel + 1);
+      }
     };
     if constexpr (MULTI) {
       const int cls = (mt - 1) * 4 + (((it.n + 7) >> 3) - 1);

@@ -114,6 +114,32 @@ def test_k_panels(oracle, ctx, monkeypatch, npanels):
         assert_parity(from_store(c), want)
 
 
+@pytest.mark.parametrize("npanels,bs", [(2, 20), (3, 23), (7, 20), (16, 8)])
+def test_k_panels_one_launch(oracle, ctx, monkeypatch, npanels, bs):
+    """One block size (a single DMMA class): all K panels run as ONE launch,
+    per-tile flags ordering the in-place accumulation.  Against the oracle,
+    and bit-identical to one launch per panel (BT_PANEL_FUSE=0: same
+    summation order)."""
+    monkeypatch.setenv("BT_KPANELS", str(npanels))
+    sizes = np.full(40, bs, np.int32)
+    ksz = np.full(120, bs, np.int32)
+    A, B, Cin = _case(oracle, 700 + npanels, sizes, ksz, sizes, 0.15, 0.15, 0.3)
+    from paper_1910_13555_b200.store import multiply_local
+    got = {}
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("BT_PANEL_FUSE", fuse)
+        for eps in (0.0, 1e-2):
+            want, nprod, _ = oracle.multiply(A, B, Cin, eps)
+            a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+            st = multiply_local(ctx, a, b, c, eps)
+            assert st["products"] == nprod
+            out = from_store(c)
+            assert_parity(out, want)
+            got[(fuse, eps)] = out
+    for eps in (0.0, 1e-2):
+        assert np.array_equal(got[("1", eps)].vals, got[("0", eps)].vals)
+
+
 @pytest.mark.parametrize("colmask,sort_min", [(1, 48), (0, 48), (0, 0), (0, 100000), (1, 0)])
 def test_emission_paths(oracle, ctx, monkeypatch, colmask, sort_min):
     """The fill pass's three product-emission paths (rank emission by column
