@@ -1016,11 +1016,17 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       const double c_bytes = 8.0 * static_cast<double>(nvals);
       int npanels = 1;
       if (ab_bytes > 2.0 * 126e6 && nitems > 0) {
+        // one DMMA class: all panels in one launch (no per-panel tail), so
+        // panels of ~100 MB of A/B (c3 sweep: 10 % best at 12-20 panels, 50 %
+        // at 64); several classes: one launch per panel, fewer and larger
+        int present = 0;
+        for (int q = 0; q < NCLASS; ++q) present += ibound[q + 1] > ibound[q];
+        const bool one = present == 1 && ibound[GENERIC + 1] == ibound[GENERIC];
         const double per_tile = static_cast<double>(nprod) / static_cast<double>(nitems);
-        int p = static_cast<int>(std::ceil(ab_bytes / 60e6));
+        int p = static_cast<int>(std::ceil(ab_bytes / (one ? 100e6 : 60e6)));
         p = std::min(p, static_cast<int>(per_tile / 4));          // >= ~4 products/panel
-        p = std::min(p, static_cast<int>(0.5 * ab_bytes / (2.0 * c_bytes)));  // C traffic
-        p = std::min(p, 32);
+        p = std::min(p, static_cast<int>((one ? 0.5 : 0.25) * ab_bytes / c_bytes));  // C traffic
+        p = std::min(p, one ? 64 : 32);
         npanels = std::max(1, p);
       }
       if (nitems > 0) npanels = std::min(64, std::max(1, env_int("BT_KPANELS", npanels)));
