@@ -72,6 +72,7 @@ struct RowArgs {
   int sort_min;   // rows with more A entries per chunk emit by window sort
   bool colmask;   // k_row_fill has a 64-bit per-column mask array (N <= kMaskCols)
   int tall_rows;  // tile height for blocks taller than 32 rows (24 or 32)
+  int splits;     // k_row_fill CTAs per C row (long rows: chunk ranges)
   bool dmma_ok;
   // pass 1 outputs
   int32_t* row_nnz;
@@ -162,11 +163,16 @@ __device__ __forceinline__ int find_entry(const RowChunk& rc, int n, int32_t t) 
 // at most kPairCap pairs, pair t's column (0xffffffff if filtered out) and B
 // tile offset are kept in shared memory so the emission sweeps need no global
 // loads; returns whether the cache is valid.
+// before / split_c0 (split fill CTAs): before[j] also counts the kept pairs of
+// the A entries ahead of split_c0 (the chunks of the earlier CTAs of the row).
 __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_t* bits,
                              RowChunk& rc, unsigned long long* cand, unsigned long long* mnk,
-                             uint32_t* cache_j = nullptr, int32_t* cache_bu = nullptr) {
+                             uint32_t* cache_j = nullptr, int32_t* cache_bu = nullptr,
+                             uint32_t* before = nullptr, int32_t split_c0 = 0) {
   const int nw = static_cast<int>((g.ncols + 31) >> 5);
   for (int64_t j = threadIdx.x; j < g.ncols; j += blockDim.x) cnt[j] = 0u;
+  if (before)
+    for (int64_t j = threadIdx.x; j < g.ncols; j += blockDim.x) before[j] = 0u;
   for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0u;
   __syncthreads();
   for (int32_t e = g.c_rp[i] + threadIdx.x; e < g.c_rp[i + 1]; e += blockDim.x) {
@@ -180,6 +186,7 @@ __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
     const int n = min(kChunkA, a1 - c0);
     const int64_t T = stage_chunk(g, c0, a1, rc);
     const bool cache = cache_j && a1 - a0 <= kChunkA && T <= kPairCap;
+    const bool ahead = before && c0 < split_c0;
     for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
       const int l = find_entry(rc, n, static_cast<int32_t>(t));
       const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
@@ -194,6 +201,7 @@ __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
         cache_bu[t] = static_cast<int32_t>(g.b_off[f] >> 6);
       }
       if (atomicAdd(&cnt[j], 1u) == 0u) atomicOr(&bits[j >> 5], 1u << (j & 31));
+      if (ahead) atomicAdd(&before[j], 1u);
       if (mnk) *mnk += static_cast<unsigned long long>(rc.ksz[l]) * g.n_sz[j];
     }
     __syncthreads();
@@ -310,10 +318,27 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   using Sort = cub::BlockRadixSort<uint32_t, kChunkA, kPairPT>;
   __shared__ typename Sort::TempStorage sort_tmp;
   __shared__ unsigned long long cls_n[NSEG], cls_at[NSEG];
-  const int64_t i = blockIdx.x;
+  // long rows: `splits` CTAs per row, CTA s emitting the products of its range
+  // of A chunks (its column cursors start after the earlier ranges' pairs);
+  // the row's C index and work items are written by CTA 0
+  const int64_t i = blockIdx.x / g.splits;
+  const int split = static_cast<int>(blockIdx.x % g.splits);
+  const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
+  const int nch = (a1 - a0 + kChunkA - 1) / kChunkA;
+  const int ch_lo = static_cast<int>((static_cast<int64_t>(split) * nch) / g.splits);
+  const int ch_hi = static_cast<int>((static_cast<int64_t>(split + 1) * nch) / g.splits);
+  if (split > 0 && ch_lo == ch_hi) return;
+  const int32_t e_lo = a0 + ch_lo * kChunkA;
+  const int32_t e_hi = min(a1, a0 + ch_hi * kChunkA);
+  uint32_t* before = nullptr;
+  if (split > 0)
+    before = sm + (g.colmask ? ((3 * g.ncols + ((g.ncols + 31) >> 5) + 1) & ~int64_t(1)) +
+                                   2 * g.ncols
+                             : 3 * g.ncols + ((g.ncols + 31) >> 5));
   for (int t = threadIdx.x; t < NSEG; t += blockDim.x) cls_n[t] = 0;
   // single-chunk rows: pair columns / B offsets cached, rc stays staged
-  const bool cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, s_key, s_bu);
+  const bool cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, s_key, s_bu, before,
+                                   e_lo);
   const int m = g.m_sz[i];
   const int32_t cbase = g.out_rp[i];
   const int64_t pbase = g.prod_base[i], vbase = g.val_base[i];
@@ -337,7 +362,8 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       __syncthreads();
       BS(tmp).ExclusiveSum(tv, v_ex, v_tot);
       __syncthreads();
-      if (ok) {
+      if (ok && split > 0) cur[j] = static_cast<int32_t>(run_prod + p_ex + before[j]);
+      if (ok && split == 0) {
         const int32_t c = cbase + q;
         g.out_col[c] = static_cast<int32_t>(j);
         g.out_row[c] = static_cast<int32_t>(i);
@@ -357,6 +383,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
     }
   }
   __syncthreads();
+  if (split == 0) {
   // reserve this row's work items in every class segment (one atomic per class)
   for (int t = threadIdx.x; t < NSEG; t += blockDim.x) {
     const unsigned long long k = cls_n[t];
@@ -389,9 +416,9 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       g.items[at + q] = it;
     }
   }
-  // products, k ascending
-  const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
-  for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
+  }  // split == 0
+  // products, k ascending (this CTA's chunks)
+  for (int32_t c0 = e_lo; c0 < e_hi; c0 += kChunkA) {
     const int n = min(kChunkA, a1 - c0);
     const int64_t T = cached ? rc.pref[n] : stage_chunk(g, c0, a1, rc);
     if (cached && g.colmask && n <= 64) {
@@ -824,6 +851,15 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     // the fill pass's rank emission needs 8 more bytes per column
     const bool colmask = N <= 4096 && env_int("BT_COLMASK", 1);
     if (colmask) row_smem = 4 * ((3 * N + (N + 31) / 32 + 1) & ~int64_t(1)) + 8 * N;
+    // few long C rows (c3: 100 rows of ~2000 A entries): several fill CTAs per
+    // row, each emitting a range of A chunks (+4 bytes per column of counts)
+    int fill_splits = 1;
+    if (M > 0 && M < 2 * x.num_sms) {
+      const int64_t chunks = (A.nblk / M + kChunkA - 1) / kChunkA;
+      fill_splits = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, chunks / 2)));
+    }
+    fill_splits = std::min(64, std::max(1, env_int("BT_FILL_SPLITS", fill_splits)));
+    if (fill_splits > 1) row_smem += 4 * static_cast<size_t>(N);
     BT_REQUIRE(row_smem <= 180 * 1024, BT_ERR_INVALID_ARGUMENT,
                "multiply: more than 15000 block columns per C row is not supported");
 
@@ -863,6 +899,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.sort_min = env_int("BT_SORT_MIN", 48);
     ra.colmask = colmask;
     ra.tall_rows = env_int("BT_TALL_ROWS", 32) == 24 ? 24 : 32;
+    ra.splits = fill_splits;
     {
       // column bands: when A and B together overflow a comfortable share of L2
       // (but are not in the K-panel regime below), sweep C in bands of B
@@ -985,7 +1022,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     if (phases) BT_CUDA(cudaEventRecord(x.ev[5], st));
     if (nout > 0) {
       ensure_dyn_smem(reinterpret_cast<const void*>(k_row_fill), row_smem);
-      k_row_fill<<<static_cast<unsigned>(M), kChunkA, row_smem, st>>>(ra);
+      k_row_fill<<<static_cast<unsigned>(M * fill_splits), kChunkA, row_smem, st>>>(ra);
       check_launch("row_fill");
       count_launch(&x);
     }

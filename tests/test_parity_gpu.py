@@ -140,6 +140,37 @@ def test_k_panels_one_launch(oracle, ctx, monkeypatch, npanels, bs):
         assert np.array_equal(got[("1", eps)].vals, got[("0", eps)].vals)
 
 
+@pytest.mark.parametrize("splits,sort_min", [(2, 48), (3, 48), (5, 100000), (8, 48)])
+def test_fill_splits(oracle, ctx, monkeypatch, splits, sort_min):
+    """Long C rows filled by several CTAs (each a range of A chunks, cursors
+    offset by the earlier ranges' pairs) emit the same descriptors: against
+    the oracle and bit-identical to one CTA per row.  Rows here hold 150 ..
+    1500 A entries (1 .. 6 chunks of 256), mixed sizes, eps filter, C_in."""
+    monkeypatch.setenv("BT_SORT_MIN", str(sort_min))
+    rng = np.random.default_rng(splits)
+    rsz = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 6)]
+    ksz = np.array([4, 20, 23], np.int32)[rng.integers(0, 3, 3000)]
+    nsz = np.array([5, 13, 23, 32], np.int32)[rng.integers(0, 4, 40)]
+    occ = np.array([0.05, 0.2, 0.5])
+    A = oracle.random_matrix(900 + splits, rsz, ksz, float(occ[splits % 3]))
+    B = oracle.random_matrix(901 + splits, ksz, nsz, 0.05)
+    Cin = oracle.random_matrix(902 + splits, rsz, nsz, 0.3)
+    from paper_1910_13555_b200.store import multiply_local
+    got = {}
+    for sp in (str(splits), "1"):
+        monkeypatch.setenv("BT_FILL_SPLITS", sp)
+        for eps in (0.0, 0.5):
+            want, nprod, _ = oracle.multiply(A, B, Cin, eps)
+            a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+            st = multiply_local(ctx, a, b, c, eps)
+            assert st["products"] == nprod
+            out = from_store(c)
+            assert_parity(out, want)
+            got[(sp, eps)] = out
+    for eps in (0.0, 0.5):
+        assert np.array_equal(got[(str(splits), eps)].vals, got[("1", eps)].vals)
+
+
 @pytest.mark.parametrize("colmask,sort_min", [(1, 48), (0, 48), (0, 0), (0, 100000), (1, 0)])
 def test_emission_paths(oracle, ctx, monkeypatch, colmask, sort_min):
     """The fill pass's three product-emission paths (rank emission by column
