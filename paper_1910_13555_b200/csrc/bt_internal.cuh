@@ -195,6 +195,18 @@ constexpr int kNormThreads = 256;
 __global__ void k_block_norms(const double* vals, const int32_t* row_ptr, const int32_t* col,
                               const int64_t* off, const int32_t* rsz, const int32_t* csz,
                               int64_t nbr, double* out, int64_t nblk);
+// the norms of two stores (A and B of a filtered multiply) in one launch:
+// warps [0, a.nblk) take A's blocks, the rest B's
+struct NormSrc {
+  const double* vals;
+  const int32_t *row_ptr, *col;
+  const int64_t* off;
+  const int32_t *rsz, *csz;
+  int64_t nbr;
+  double* out;
+  int64_t nblk;
+};
+__global__ void k_block_norms_pair(NormSrc a, NormSrc b);
 void upload_sizes(Mat& m);
 void check_launch(const char* what);
 // integer environment knob (development / experiments), default when unset

@@ -868,12 +868,13 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     if (eps > 0 && A.nblk && B.nblk) {
       na.alloc(A.nblk, st);
       nb.alloc(B.nblk, st);
-      k_block_norms<<<blocks_for(A.nblk * 32, kNormThreads), kNormThreads, 0, st>>>(
-          A.vals.p, A.row_ptr.p, A.col.p, A.off.p, A.rsz.p, A.csz.p, A.nbr, na.p, A.nblk);
-      k_block_norms<<<blocks_for(B.nblk * 32, kNormThreads), kNormThreads, 0, st>>>(
-          B.vals.p, B.row_ptr.p, B.col.p, B.off.p, B.rsz.p, B.csz.p, B.nbr, nb.p, B.nblk);
+      // one launch for both stores: half the tail of two separate grids
+      const NormSrc sa{A.vals.p, A.row_ptr.p, A.col.p, A.off.p, A.rsz.p, A.csz.p, A.nbr, na.p, A.nblk};
+      const NormSrc sb{B.vals.p, B.row_ptr.p, B.col.p, B.off.p, B.rsz.p, B.csz.p, B.nbr, nb.p, B.nblk};
+      k_block_norms_pair<<<blocks_for((A.nblk + B.nblk) * 32, kNormThreads), kNormThreads, 0, st>>>(
+          sa, sb);
       check_launch("block_norms");
-      count_launch(&x, 2);
+      count_launch(&x);
     }
 
     const int kmax = A.max_c;

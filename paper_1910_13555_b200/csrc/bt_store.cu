@@ -237,13 +237,13 @@ __global__ void k_compact(double* __restrict__ dst, const int64_t* __restrict__ 
 // gives identical bits.  One warp per block, one lane per row (32 rows at a
 // time): the dependent chain is n + m additions, not m * n.
 // Launch with kNormThreads threads per CTA.
-__global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __restrict__ row_ptr,
-                              const int32_t* __restrict__ col, const int64_t* __restrict__ off,
-                              const int32_t* __restrict__ rsz, const int32_t* __restrict__ csz,
-                              int64_t nbr, double* __restrict__ out, int64_t nblk) {
-  const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (b >= nblk) return;
+__device__ __forceinline__ void block_norm(const double* __restrict__ vals,
+                                           const int32_t* __restrict__ row_ptr,
+                                           const int32_t* __restrict__ col,
+                                           const int64_t* __restrict__ off,
+                                           const int32_t* __restrict__ rsz,
+                                           const int32_t* __restrict__ csz, int64_t nbr,
+                                           double* __restrict__ out, int64_t b, int lane) {
   // row of entry b (last r with row_ptr[r] <= b): 32-way search, one probe
   // per lane per step, so ~log32(nbr) dependent loads instead of log2(nbr)
   int64_t lo = 0, hi = nbr;  // row_ptr[lo] <= b < row_ptr[hi]
@@ -289,6 +289,25 @@ __global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __
     for (int k = 0; k < cnt; ++k) s = __dadd_rn(s, __shfl_sync(0xffffffffu, rs, k));
   }
   if (lane == 0) out[b] = __dsqrt_rn(s);
+}
+
+__global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __restrict__ row_ptr,
+                              const int32_t* __restrict__ col, const int64_t* __restrict__ off,
+                              const int32_t* __restrict__ rsz, const int32_t* __restrict__ csz,
+                              int64_t nbr, double* __restrict__ out, int64_t nblk) {
+  const int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (b >= nblk) return;
+  block_norm(vals, row_ptr, col, off, rsz, csz, nbr, out, b, threadIdx.x & 31);
+}
+
+__global__ void k_block_norms_pair(NormSrc a, NormSrc b) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w < a.nblk) {
+    block_norm(a.vals, a.row_ptr, a.col, a.off, a.rsz, a.csz, a.nbr, a.out, w, lane);
+  } else if (w - a.nblk < b.nblk) {
+    block_norm(b.vals, b.row_ptr, b.col, b.off, b.rsz, b.csz, b.nbr, b.out, w - a.nblk, lane);
+  }
 }
 
 // ------------------------------------------------------------- host helpers
