@@ -300,7 +300,10 @@ __global__ void k_block_norms(const double* __restrict__ vals, const int32_t* __
   block_norm(vals, row_ptr, col, off, rsz, csz, nbr, out, b, threadIdx.x & 31);
 }
 
-__global__ void k_block_norms_pair(NormSrc a, NormSrc b) {
+// latency-bound (a few dependent loads per warp): occupancy hides it best, so
+// 8 CTAs of 256 threads per SM (32 registers; a per-warp preload variant with
+// 72 registers was 40 % slower, profiles/r01d/norms_preload_ab.txt)
+__global__ void __launch_bounds__(256, 8) k_block_norms_pair(NormSrc a, NormSrc b) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w < a.nblk) {
