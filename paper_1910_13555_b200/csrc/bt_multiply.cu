@@ -611,12 +611,31 @@ __global__ void k_panel_items(const Item* __restrict__ base, int64_t nitems,
 
 // Work-item segment bases (exclusive scan of the per-segment counts) and zeroed
 // ticket counters, written on the device: no host round trip before the fill.
-__device__ void init_cursors(const unsigned long long* seg_items, unsigned long long* cursor) {
-  if (threadIdx.x == 0) {
-    unsigned long long run = 0;
-    for (int q = 0; q < NSEG; ++q) {
-      cursor[q] = run;
-      run += seg_items[q];
+// Warp 0 scans: lane l owns NSEG/32 consecutive segments (all loads issued at
+// once), then a shuffle scan of the lane sums -- instead of one thread walking
+// NSEG dependent entries.  Needs blockDim.x >= 32.
+__device__ void init_cursors(const unsigned long long* __restrict__ seg_items,
+                             unsigned long long* __restrict__ cursor) {
+  constexpr int kPer = (NSEG + 31) / 32;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x, q0 = lane * kPer;
+    unsigned long long v[kPer], sum = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      v[j] = q0 + j < NSEG ? seg_items[q0 + j] : 0ull;
+      sum += v[j];
+    }
+    unsigned long long incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    unsigned long long run = incl - sum;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      if (q0 + j < NSEG) cursor[q0 + j] = run;
+      run += v[j];
     }
   }
   for (int q = threadIdx.x; q < NCLASS; q += blockDim.x) cursor[NSEG + q] = 0ull;
