@@ -275,19 +275,30 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
     agg_add(&cls_items[seg], seg,
             static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
   }
-  using BR = cub::BlockReduce<long long, kChunkA>;
-  __shared__ typename BR::TempStorage tmp;
-  const long long t_nnz = BR(tmp).Sum(nnz);
+  // the six row sums in one reduction: shuffles within each warp, one
+  // barrier, then thread 0 adds the per-warp partials (exact integer sums)
+  constexpr int kW = kChunkA / 32;
+  __shared__ long long part[6][kW];
+  long long r6[6] = {nnz, prods, vals, elems, static_cast<long long>(cand),
+                     static_cast<long long>(mnk)};
+#pragma unroll
+  for (int q = 0; q < 6; ++q)
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) r6[q] += __shfl_xor_sync(0xffffffffu, r6[q], d);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) part[q][threadIdx.x >> 5] = r6[q];
+  }
   __syncthreads();
-  const long long t_prod = BR(tmp).Sum(prods);
-  __syncthreads();
-  const long long t_vals = BR(tmp).Sum(vals);
-  __syncthreads();
-  const long long t_el = BR(tmp).Sum(elems);
-  __syncthreads();
-  const long long t_cand = BR(tmp).Sum(static_cast<long long>(cand));
-  __syncthreads();
-  const long long t_mnk = BR(tmp).Sum(static_cast<long long>(mnk));
+  long long tq[6] = {0, 0, 0, 0, 0, 0};
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int w = 0; w < kW; ++w) tq[q] += part[q][w];
+  }
+  const long long t_nnz = tq[0], t_prod = tq[1], t_vals = tq[2], t_el = tq[3], t_cand = tq[4],
+                  t_mnk = tq[5];
   if (threadIdx.x == 0) {
     g.row_nnz[i] = static_cast<int32_t>(t_nnz);
     g.row_prod[i] = t_prod;
