@@ -358,8 +358,12 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   {
     // touched columns in ascending order, 256 at a time: ranks, product bases
     // and T8 offsets by block scans
-    using BS = cub::BlockScan<long long, kChunkA>;
-    __shared__ typename BS::TempStorage tmp;
+    // both exclusive scans at once: warp shuffles, then the per-warp totals
+    // through shared memory (2 barriers per 256 columns instead of two cub
+    // block scans with their own barriers)
+    constexpr int kW = kChunkA / 32;
+    __shared__ long long wt[2][kW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     long long run_prod = 0, run_val = 0;
     for (int q0 = 0; q0 < ntouch; q0 += blockDim.x) {
       const int q = q0 + threadIdx.x;
@@ -368,10 +372,32 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       const uint32_t cj = ok ? cnt[j] : 0u;
       const int n = ok ? g.n_sz[j] : 0;
       const long long np = cj & ~kCinFlag, tv = ok ? t8_size(m, n) : 0;
-      long long p_ex, v_ex, p_tot, v_tot;
-      BS(tmp).ExclusiveSum(np, p_ex, p_tot);
+      long long pi = np, vi = tv;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const long long py = __shfl_up_sync(0xffffffffu, pi, d);
+        const long long vy = __shfl_up_sync(0xffffffffu, vi, d);
+        if (lane >= d) {
+          pi += py;
+          vi += vy;
+        }
+      }
+      if (lane == 31) {
+        wt[0][wid] = pi;
+        wt[1][wid] = vi;
+      }
       __syncthreads();
-      BS(tmp).ExclusiveSum(tv, v_ex, v_tot);
+      long long p_ex = pi - np, v_ex = vi - tv, p_tot = 0, v_tot = 0;
+#pragma unroll
+      for (int w = 0; w < kW; ++w) {
+        const long long a = wt[0][w], b = wt[1][w];
+        if (w < wid) {
+          p_ex += a;
+          v_ex += b;
+        }
+        p_tot += a;
+        v_tot += b;
+      }
       __syncthreads();
       if (ok && split > 0) cur[j] = static_cast<int32_t>(run_prod + p_ex + before[j]);
       if (ok && split == 0) {
