@@ -44,6 +44,21 @@ FP64_PEAK_TFLOPS = 37.1   # measured: tools/microbench/fp64_peak.cu on B200 (pro
 NCU_TRAFFIC_BYTES = 1.316e9
 
 
+METRIC = "block-sparse FP64 useful GFLOP/s"
+DATA = "synthetic (seeded Bernoulli(0.10) block presence, N(0,1) values)"
+
+
+def bench_config(world, products_per_rank, flops_per_rank, distribution, l2):
+    """The `config` object of both arms (same keys, same workload string)."""
+    return {
+        "workload": "c1: 400x400 blocks of 23x23 (N=9200) per rank, occ 0.10, C_in empty, eps 0",
+        "products_per_rank": int(products_per_rank),
+        "useful_gflop_per_rank": round(flops_per_rank / 1e9, 4),
+        "distribution": distribution,
+        "l2": l2,
+    }
+
+
 # --------------------------------------------------------------- inputs
 def make_blocks(seed: int, nbr: int, nbc: int, bs: int, occ: float, row0: int = 0):
     """Canonical (bi, bj, vals) block list, Bernoulli(occ) presence, N(0,1) values.
@@ -132,8 +147,8 @@ def run_reference(args, rank, world):
         return None
     from oracle.oracle import Blocks, Reference  # the one place bench runs oracle/
     ref = Reference()
-    cores = os.cpu_count() or 1
-    q = int(np.floor(np.sqrt(cores)))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    q = int(np.floor(np.sqrt(cores or 1)))
     sz = np.full(NB, BS, np.int32)
     abi, abj, av = make_blocks(SEED_A, NB, NB, BS, OCC)
     bbi, bbj, bv = make_blocks(SEED_B, NB, NB, BS, OCC)
@@ -141,6 +156,7 @@ def run_reference(args, rank, world):
     B = Blocks(sz, sz, bbi, bbj, bv)
     C = Blocks.empty(sz, sz)
     flops = useful_flops_host(abi, abj, bbi, bbj, BS)
+    nprod = flops / (2.0 * BS ** 3)
     for _ in range(args.warmup):
         ref.multiply(A, B, C, "cannon", q, q * q)
     times = []
@@ -150,13 +166,17 @@ def run_reference(args, rank, world):
     t = float(np.sum(times))
     val = flops * args.steps / t / 1e9
     line = {
-        "impl": "reference", "metric": "block-sparse FP64 useful GFLOP/s",
+        "impl": "reference", "metric": METRIC,
         "value": round(val, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Bernoulli presence, N(0,1) values)",
-        "config": {"workload": "c1: 400x400 blocks of 23x23 (N=9200), occ 0.10, eps 0",
-                   "algorithm": f"reference multiply_cannon on a {q}x{q} simulated grid"},
+        "data": DATA,
+        "config": bench_config(world, int(nprod), flops,
+                               f"reference multiply_cannon on a {q}x{q} simulated grid "
+                               f"({q * q} host threads); each step is one c1 instance "
+                               f"(rank 0's slab of the {world}-rank job)",
+                               "n/a (CPU reference; the host caches hold nothing across "
+                               "the 15 GFLOP step)"),
         "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": q * q,
                          "kind": "reference",
                          "sample": f"full c1 instance per step ({flops/1e9:.2f} GFLOP)"},
@@ -188,6 +208,44 @@ def cpu_baseline_sample(reps: int = 3):
 
 
 # --------------------------------------------------------------- product
+def relaunch_under_torchrun(n: int):
+    """`bench.py --gpus N` without a launcher: re-exec as N ranks (one process per
+    GPU) under torch.distributed.run on 127.0.0.1, NCCL's init lines visible."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    os.execvpe(sys.executable, cmd, env)
+
+
+def parity_vs_reference(c_store, ref_c):
+    """The bench's own GPU C (rank 0's slab) against the reference's C for the same
+    inputs: pattern bit-exact, per-block and global Frobenius-relative error
+    (oracles.hpp:49-57; north_star bar 1e-12)."""
+    bi, bj, v = c_store.export()
+    exact = bool(len(bi) == ref_c.nblk and np.array_equal(bi, ref_c.bi)
+                 and np.array_equal(bj, ref_c.bj) and v.shape == ref_c.vals.shape)
+    out = {"pattern_exact": exact, "blocks": int(len(bi)),
+           "checked": "rank 0's C vs the reference multiply_cannon (1x1) on the same inputs"}
+    if exact:
+        d = (v - ref_c.vals) ** 2
+        r = ref_c.vals ** 2
+        off = ref_c.offsets()[:-1]
+        per = np.sqrt(np.add.reduceat(d, off) / np.maximum(np.add.reduceat(r, off), 1e-300))
+        out["max_frob"] = float(per.max()) if len(per) else 0.0
+        out["global_frob"] = float(np.sqrt(d.sum() / r.sum())) if r.sum() > 0 else 0.0
+        out["ok"] = out["max_frob"] <= 1e-12
+    else:
+        out["ok"] = False
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -195,12 +253,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="N > 1: skip rank 0's check against the reference")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        relaunch_under_torchrun(args.gpus)   # does not return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "b200" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -374,30 +438,41 @@ def main():
         e2e_s = float(t.item())
     e2e_val = flops_step * world / e2e_s / 1e9
 
+    # ---- parity of this run's own C (rank 0's slab) against the reference
+    ref_out = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:   # rank 0 at N = 1 only
+        cb, ref_out = cpu_baseline_sample()
+    elif rank == 0 and not args.no_parity:
+        from oracle.oracle import Blocks, Reference   # the checker, after the timed region
+        q = max(1, int(np.floor(np.sqrt(len(os.sched_getaffinity(0))))))
+        A = Blocks(sz, sz, abi, abj, av)
+        B = Blocks(sz, sz, bbi_all, bbj_all, bv_all)
+        ref_out, _, _ = Reference().multiply(A, B, Blocks.empty(sz, sz), "cannon", q, q * q)
+    parity = None
+    if ref_out is not None:
+        parity = parity_vs_reference(c if world == 1 else c.local(rank), ref_out)
+
+    line = None
     if rank == 0:
+        dist_desc = ("single GPU" if world == 1 else
+                     f"case 2 weak scaling: A/C 400-block-row slabs per rank, B K-slabs "
+                     f"gathered over NVLink/NCCL each step ({world} ranks)")
         line = {
-            "metric": "block-sparse FP64 useful GFLOP/s",
+            "metric": METRIC,
             "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Bernoulli(0.10) block presence, N(0,1) values)",
-            "config": {
-                "workload": "c1: 400x400 blocks of 23x23 (N=9200) per rank, occ 0.10, "
-                            "C_in empty, eps 0",
-                "products_per_rank": int(stats[-1]["products"]),
-                "useful_gflop_per_rank": round(flops_step / 1e9, 4),
-                "distribution": "single GPU" if world == 1 else
-                f"case 2 weak scaling: A/C 400-block-row slabs per rank, B K-slabs "
-                f"gathered over NVLink/NCCL each step ({world} ranks)",
-                "l2": "flushed (256 MB write) before every timed step",
-            },
+            "data": DATA,
+            "config": bench_config(world, stats[-1]["products"], flops_step, dist_desc,
+                                   "flushed (256 MB write) before every timed step"),
             "roofline": {
                 "bound": "tensor", "achieved": round(achieved, 3),
                 "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
                 "traffic": NCU_TRAFFIC_BYTES if world == 1 else None,
                 "traffic_note": "DRAM bytes per launch (ncu); algorithmic bytes "
-                                f"{alg_bytes / 1e9:.3f} GB (8*(|A|+|B|+|C|) T8 slabs + index)",
+                                f"{alg_bytes / 1e9:.3f} GB (8*(|A|+|B|+|C|) unpadded elements "
+                                "+ 12 B index per block)",
                 "kernel": "k_smm_dmma<3,3,4,1> (FP64 DMMA 8x8x4 small-GEMM, T8 tiles, "
                           "bulk-async staged)",
                 "peak_source": "measured FP64 DMMA/DFMA peak on B200 "
@@ -409,10 +484,10 @@ def main():
             "gpu_launches": int(kernels),
             "clocks": clocks.summary(),
         }
-        if not args.no_cpu_baseline and world == 1:   # rank 0 at N = 1 only
-            cb, _ = cpu_baseline_sample()
+        if parity is not None:
+            line["parity"] = parity
+        if world == 1 and ref_out is not None:
             line["cpu_baseline"] = cb
-        print(json.dumps(line), flush=True)
     if world > 1:
         comm.close()
     else:
@@ -421,6 +496,10 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+    if line is not None:   # last: after NCCL's teardown output
+        print(json.dumps(line), flush=True)
+        if parity is not None and not parity["ok"]:
+            sys.exit("bench.py: parity check against the reference FAILED")
 
 
 if __name__ == "__main__":

@@ -125,6 +125,11 @@ int bt_multiply(bt_ctx* ctx, const bt_mat* a, const bt_mat* b, bt_mat* c, double
 
 /* Post-filter: drops C blocks with ||C_ij||_F < eps. */
 int bt_filter(bt_mat* m, double eps);
+/* bt_filter that also reports: *dropped = blocks removed, *borderline = blocks
+ * with | ||C_ij||_F - eps | <= band * eps, whose keep/drop decision could flip
+ * under ULP-level value differences (e.g. band = 1e-12).
+ * dropped / borderline may be NULL. */
+int bt_filter_report(bt_mat* m, double eps, double band, int64_t* dropped, int64_t* borderline);
 
 /* ------------------------------------------------------ distributed layer */
 typedef struct bt_grid bt_grid; /* process group + ledger: SimComm (comm.hpp:152-397) */

@@ -95,6 +95,8 @@ class Oracle:
         L.bto_multiply.argtypes = [C.POINTER(_BtoMat), C.POINTER(_BtoMat), C.POINTER(_BtoMat),
                                    C.c_double, _i64p, _f64p]
         L.bto_filter.argtypes = [C.POINTER(_BtoMat), C.c_double]
+        L.bto_block_norm.argtypes = [_f64p, C.c_int, C.c_int]
+        L.bto_block_norm.restype = C.c_double
         L.bto_block_gemm_acc.argtypes = [_f64p, _f64p, _f64p, C.c_int, C.c_int, C.c_int]
         L.bto_rng_seed.argtypes = [C.c_void_p, C.c_uint64]
         L.bto_rng_next.argtypes = [C.c_void_p]
@@ -168,6 +170,17 @@ class Oracle:
         self.lib.bto_filter(C.byref(mc), eps)
         out = self._from(mc)
         self.lib.bto_mat_free(C.byref(mc))
+        return out
+
+    def norms(self, c: Blocks) -> np.ndarray:
+        """Block Frobenius norms in canonical order (bto_block_norm: sequential,
+        unfused row sums -- the filter's definition)."""
+        off = c.offsets()
+        v = np.ascontiguousarray(c.vals, np.float64)
+        out = np.zeros(c.nblk)
+        for t in range(c.nblk):
+            m, n = int(c.rsz[c.bi[t]]), int(c.csz[c.bj[t]])
+            out[t] = self.lib.bto_block_norm(v[off[t]:].ctypes.data_as(_f64p), m, n)
         return out
 
     def block_gemm_acc(self, c, a, b):

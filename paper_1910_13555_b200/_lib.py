@@ -92,6 +92,7 @@ SIGNATURES = {
     "bt_multiply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
                               C.POINTER(BtStats)]),
     "bt_filter": (C.c_int, [C.c_void_p, C.c_double]),
+    "bt_filter_report": (C.c_int, [C.c_void_p, C.c_double, C.c_double, _i64p, _i64p]),
     "bt_grid_create": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "bt_grid_destroy": (C.c_int, [C.c_void_p]),
     "bt_grid_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),

@@ -284,6 +284,7 @@ void merge_into(Mat& dst, const std::vector<Contribution>& parts, bool accumulat
   dst.col = std::move(cl);
   dst.off = std::move(of);
   dst.nblk = nout;
+  dst.norms_ok = false;
   dst.nvals = nv;
   dst.nelems = ne;
 }
@@ -418,6 +419,7 @@ void split_by_owner(Ctx& x, const Mat& s, const int32_t* d_owner, int P,
       check_launch("split_rowptr");
       count_launch(&x, 2);
       b.nblk = nd;
+      b.norms_ok = false;
       b.nvals = nv;
       b.nelems = static_cast<int64_t>(h[2 * P + d]);
     }
@@ -575,6 +577,7 @@ void exchange(Grid& g, const std::vector<Send>& sends, const std::vector<Recv>& 
   for (size_t q = 0; q < nr; ++q) {
     Mat& d = *peer_recvs[q]->dst;
     d.nblk = hdr[3 * (ns + q)];
+    d.norms_ok = false;
     d.nvals = hdr[3 * (ns + q) + 1];
     d.nelems = hdr[3 * (ns + q) + 2];
     d.row_ptr.alloc(d.nbr + 1, g.comm);
@@ -632,6 +635,7 @@ void copy_store(const Mat& s, Mat& d) {
     BT_CUDA(cudaMemcpyAsync(d.vals.p, s.vals.p, 8 * s.nvals, cudaMemcpyDeviceToDevice, st));
   }
   d.nblk = s.nblk;
+  d.norms_ok = false;
   d.nvals = s.nvals;
   d.nelems = s.nelems;
 }
@@ -899,6 +903,7 @@ void concat_rows(const std::vector<const Mat*>& parts, const std::vector<int32_t
   out.off = std::move(off);
   out.vals = std::move(vals);
   out.nblk = nblk;
+  out.norms_ok = false;
   out.nvals = nvals;
   out.nelems = nel;
 }
@@ -945,6 +950,7 @@ cudaEvent_t gather_rows_nccl(Grid& g, const Mat& mine, const std::vector<int32_t
   grow(full.off, static_cast<size_t>(std::max<int64_t>(bb[nprocs], 1)));
   grow(full.vals, static_cast<size_t>(std::max<int64_t>(vb[nprocs], 64)));
   full.nblk = bb[nprocs];
+  full.norms_ok = false;
   full.nvals = vb[nprocs];
   full.nelems = nel;
   if (static_cast<int>(g.gather_rps.size()) < nprocs) g.gather_rps.resize(nprocs);
@@ -1093,6 +1099,7 @@ void gather_check(Grid& g, const Mat& mine, int nprocs, Mat& full, bool spec) {
     g.spec_capv = (maxv / 2) & ~int64_t(63);
   }
   full.nblk = nblk;
+  full.norms_ok = false;
   full.nelems = nel;
   const int me = g.first;
   g.charge_send(me, (nprocs - 1) * mine.nelems, (nprocs - 1) * 4 * mine.nblk);
@@ -1176,6 +1183,7 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
   grow(full.off, static_cast<size_t>(std::max<int64_t>(maxb * nprocs, 1)));
   grow(full.vals, static_cast<size_t>(std::max<int64_t>(maxv * nprocs, 64)));
   full.nblk = maxb * nprocs;  // upper bound until the sizes are known (gather_check)
+  full.norms_ok = false;
   full.nvals = maxv * nprocs;
   full.nelems = 0;
   BT_CUDA(cudaEventRecord(g.ev_main, x.stream));

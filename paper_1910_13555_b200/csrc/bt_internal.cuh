@@ -155,6 +155,13 @@ struct Mat {
   DBuf<int32_t> col;
   DBuf<int64_t> off;
   DBuf<double> vals;
+  // Block Frobenius norms in storage order (eps filter), computed
+  // on first use and kept with the data: every site that changes the pattern
+  // or the values assigns nblk and clears norms_ok right after.
+  mutable DBuf<double> norm_cache;
+  mutable bool norms_ok = false;
+  // device pointer to this store's block norms (computed on `st` when stale)
+  const double* norms(cudaStream_t st) const;
   cudaStream_t stream() const { return ctx->stream; }
   void init_empty();  // empty pattern (row_ptr all zero)
   // empty pattern, keeping col/off/vals allocated as capacity for the next

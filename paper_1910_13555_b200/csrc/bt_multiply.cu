@@ -915,22 +915,33 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       fill_splits = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, chunks / 2)));
     }
     fill_splits = std::min(64, std::max(1, env_int("BT_FILL_SPLITS", fill_splits)));
-    if (fill_splits > 1) row_smem += 4 * static_cast<size_t>(N);
     BT_REQUIRE(row_smem <= 180 * 1024, BT_ERR_INVALID_ARGUMENT,
                "multiply: more than 15000 block columns per C row is not supported");
+    // split CTAs need 4 more bytes per column; rows too wide for that fall
+    // back to one CTA per row instead of failing
+    if (fill_splits > 1 && row_smem + 4 * static_cast<size_t>(N) > 180 * 1024) fill_splits = 1;
+    if (fill_splits > 1) row_smem += 4 * static_cast<size_t>(N);
 
-    // ---- norms for the eps filter
-    DBuf<double> na, nb;
+    // ---- norms for the eps filter, cached with the stores: a
+    // store's norms are computed once after it changes (both in one launch
+    // when A and B are both stale)
+    const double *na = nullptr, *nb = nullptr;
     if (eps > 0 && A.nblk && B.nblk) {
-      na.alloc(A.nblk, st);
-      nb.alloc(B.nblk, st);
-      // one launch for both stores: half the tail of two separate grids
-      const NormSrc sa{A.vals.p, A.row_ptr.p, A.col.p, A.off.p, A.rsz.p, A.csz.p, A.nbr, na.p, A.nblk};
-      const NormSrc sb{B.vals.p, B.row_ptr.p, B.col.p, B.off.p, B.rsz.p, B.csz.p, B.nbr, nb.p, B.nblk};
-      k_block_norms_pair<<<blocks_for((A.nblk + B.nblk) * 32, kNormThreads), kNormThreads, 0, st>>>(
-          sa, sb);
-      check_launch("block_norms");
-      count_launch(&x);
+      if (!A.norms_ok && !B.norms_ok && &A != &B) {
+        if (A.norm_cache.n < static_cast<size_t>(A.nblk)) A.norm_cache.alloc(A.nblk, st);
+        if (B.norm_cache.n < static_cast<size_t>(B.nblk)) B.norm_cache.alloc(B.nblk, st);
+        const NormSrc sa{A.vals.p, A.row_ptr.p, A.col.p, A.off.p, A.rsz.p, A.csz.p, A.nbr,
+                         A.norm_cache.p, A.nblk};
+        const NormSrc sb{B.vals.p, B.row_ptr.p, B.col.p, B.off.p, B.rsz.p, B.csz.p, B.nbr,
+                         B.norm_cache.p, B.nblk};
+        k_block_norms_pair<<<blocks_for((A.nblk + B.nblk) * 32, kNormThreads), kNormThreads, 0, st>>>(
+            sa, sb);
+        check_launch("block_norms");
+        count_launch(&x);
+        A.norms_ok = B.norms_ok = true;
+      }
+      na = A.norms(st);
+      nb = B.norms(st);
     }
 
     const int kmax = A.max_c;
@@ -948,8 +959,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.m_sz = Cm.rsz.p;
     ra.n_sz = Cm.csz.p;
     ra.k_sz = A.csz.p;
-    ra.na = na.p;
-    ra.nb = nb.p;
+    ra.na = na;
+    ra.nb = nb;
     ra.eps = eps;
     ra.ncols = N;
     ra.dmma_ok = dmma_ok;
@@ -1268,6 +1279,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     Cm.col = std::move(out_col);
     Cm.off = std::move(out_off);
     Cm.nblk = nout;
+    Cm.norms_ok = false;
     Cm.nvals = nvals;
     Cm.nelems = nelems;
     if (x.timing) BT_CUDA(cudaEventRecord(x.ev[3], st));

@@ -415,17 +415,25 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
 }
 
 // Generic small-GEMM (n > 32 or k > 64): one CTA per C block, one thread per
-// element, T8 operands, products in k order.
+// element, T8 operands, products in k order.  Every position of the T8 slot is
+// written -- the padding with zeros -- because the output slab is not cleared
+// beforehand and norms, the eps filter and later DMMA reads of this block as an
+// operand all rely on zero padding.
 __global__ void k_smm_generic(const NumArgs g) {
   const int64_t id = g.item_lo + blockIdx.x;
   if (blockIdx.x >= g.nitems) return;
   const Item it = g.items[id];
   const int m = it.rows, n = it.n;
-  const int NT = tiles8(n);
+  const int NT = tiles8(n), MT = tiles8(m);
   const int64_t p0 = item_p0(it);
-  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
-    const int r = e / n, q = e - r * n;
+  const int padded = MT * 8 * NT * 8;
+  for (int e = threadIdx.x; e < padded; e += blockDim.x) {
+    const int r = e / (NT * 8), q = e - r * (NT * 8);
     const int64_t cp = t8_pos(r, q, NT);
+    if (r >= m || q >= n) {
+      g.cout[it.c_off + cp] = 0.0;
+      continue;
+    }
     double acc = it.cin_off >= 0 ? g.cin[it.cin_off + cp] : 0.0;
     for (int p = 0; p < it.np; ++p) {
       const Desc d = g.desc[p0 + p];

@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <ctime>
@@ -125,6 +126,7 @@ void upload_sizes(Mat& m) {
 
 void Mat::clear_keep_capacity() {
   nblk = 0;
+  norms_ok = false;
   nelems = 0;
   nvals = 0;
   if (row_ptr.n < static_cast<size_t>(nbr + 1)) row_ptr.alloc(nbr + 1, stream());
@@ -133,6 +135,7 @@ void Mat::clear_keep_capacity() {
 
 void Mat::init_empty() {
   nblk = 0;
+  norms_ok = false;
   nelems = 0;
   nvals = 0;
   col.release();
@@ -313,6 +316,20 @@ __global__ void __launch_bounds__(256, 8) k_block_norms_pair(NormSrc a, NormSrc 
   }
 }
 
+const double* Mat::norms(cudaStream_t st) const {
+  if (nblk == 0) return nullptr;
+  if (!norms_ok || norm_cache.n < static_cast<size_t>(nblk)) {
+    if (norm_cache.n < static_cast<size_t>(nblk)) norm_cache.alloc(nblk, st);
+    k_block_norms<<<static_cast<unsigned>((nblk * 32 + kNormThreads - 1) / kNormThreads),
+                    kNormThreads, 0, st>>>(vals.p, row_ptr.p, col.p, off.p, rsz.p, csz.p, nbr,
+                                           norm_cache.p, nblk);
+    check_launch("block_norms");
+    count_launch(ctx);
+    norms_ok = true;
+  }
+  return norm_cache.p;
+}
+
 // ------------------------------------------------------------- host helpers
 struct HostIndex {
   std::vector<int32_t> row_ptr, col;
@@ -371,6 +388,7 @@ static void install_pattern(Mat& m, const std::vector<int32_t>& row_ptr,
   void* const dst[3] = {m.row_ptr.p, m.col.p, m.off.p};
   upload_parts(*m.ctx, parts, 3, dst);
   m.nblk = static_cast<int64_t>(col.size());
+  m.norms_ok = false;
   m.nvals = nvals;
   m.nelems = nelems;
 }
@@ -588,6 +606,7 @@ int bt_mat_copy(const bt_mat* src, bt_mat* dst) {
                               cudaMemcpyDeviceToDevice, st));
     }
     d.nblk = s.nblk;
+    d.norms_ok = false;
     d.nvals = s.nvals;
     d.nelems = s.nelems;
   });
@@ -854,38 +873,41 @@ int bt_mat_norms(const bt_mat* mh, double* out) {
     BT_REQUIRE(out || m.nblk == 0, BT_ERR_INVALID_ARGUMENT, "null output");
     if (m.nblk == 0) return;
     cudaStream_t st = m.stream();
-    DBuf<double> d(m.nblk, st);
-    k_block_norms<<<static_cast<unsigned>((m.nblk * 32 + kNormThreads - 1) / kNormThreads),
-                    kNormThreads, 0, st>>>(
-        m.vals.p, m.row_ptr.p, m.col.p, m.off.p, m.rsz.p, m.csz.p, m.nbr, d.p, m.nblk);
-    check_launch("block_norms");
-    count_launch(m.ctx);
-    BT_CUDA(cudaMemcpyAsync(out, d.p, sizeof(double) * m.nblk, cudaMemcpyDeviceToHost, st));
+    const double* d = m.norms(st);
+    BT_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * m.nblk, cudaMemcpyDeviceToHost, st));
     BT_CUDA(cudaStreamSynchronize(st));
   });
 }
 
-int bt_filter(bt_mat* mh, double eps) {
+int bt_filter(bt_mat* mh, double eps) { return bt_filter_report(mh, eps, 0.0, nullptr, nullptr); }
+
+int bt_filter_report(bt_mat* mh, double eps, double band, int64_t* dropped,
+                     int64_t* borderline) {
   return guard([&] {
     check_mat(mh);
     Mat& m = mh->impl;
+    BT_REQUIRE(band >= 0, BT_ERR_INVALID_ARGUMENT, "filter: negative borderline band");
+    if (dropped) *dropped = 0;
+    if (borderline) *borderline = 0;
     if (m.nblk == 0 || !(eps > 0)) return;
     cudaStream_t st = m.stream();
     std::vector<double> nrm(m.nblk);
-    DBuf<double> d(m.nblk, st);
-    k_block_norms<<<static_cast<unsigned>((m.nblk * 32 + kNormThreads - 1) / kNormThreads),
-                    kNormThreads, 0, st>>>(
-        m.vals.p, m.row_ptr.p, m.col.p, m.off.p, m.rsz.p, m.csz.p, m.nbr, d.p, m.nblk);
-    check_launch("block_norms");
-    count_launch(m.ctx);
-    BT_CUDA(cudaMemcpyAsync(nrm.data(), d.p, sizeof(double) * m.nblk, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaMemcpyAsync(nrm.data(), m.norms(st), sizeof(double) * m.nblk,
+                            cudaMemcpyDeviceToHost, st));
     HostIndex h = download_index(m);
     std::vector<int32_t> row_ptr(m.nbr + 1, 0), col;
     std::vector<int64_t> off, src, len;
     int64_t nv = 0, ne = 0;
+    int64_t n_drop = 0, n_border = 0;
     for (int64_t i = 0; i < m.nbr; ++i)
       for (int32_t e = h.row_ptr[i]; e < h.row_ptr[i + 1]; ++e) {
-        if (nrm[e] < eps) continue;
+        // borderline: a ULP-level difference in the block's values could flip
+        // the decision ("Filter semantics")
+        if (std::fabs(nrm[e] - eps) <= band * eps) ++n_border;
+        if (nrm[e] < eps) {
+          ++n_drop;
+          continue;
+        }
         const int64_t L = int64_t(m.h_rsz[i]) * m.h_csz[h.col[e]];
         const int64_t T = t8_size(m.h_rsz[i], m.h_csz[h.col[e]]);
         col.push_back(h.col[e]);
@@ -911,6 +933,8 @@ int bt_filter(bt_mat* mh, double eps) {
     m.vals = std::move(nvals);
     install_pattern(m, row_ptr, col, off, nv, ne);
     BT_CUDA(cudaStreamSynchronize(st));
+    if (dropped) *dropped = n_drop;
+    if (borderline) *borderline = n_border;
   });
 }
 

@@ -235,6 +235,7 @@ extern "C" int bt_tensor_remap(bt_ctx* ctx, int ndim, const int64_t* nblocks,
     D.col = std::move(col);
     D.off = std::move(d_off);
     D.nblk = n;
+    D.norms_ok = false;
     D.nvals = nv;
     D.nelems = ne;
     BT_CUDA(cudaStreamSynchronize(st));

@@ -173,8 +173,13 @@ class LocalStore:
     def copy_from(self, other: "LocalStore"):
         check(self.lib.bt_mat_copy(other.h, self.h), "copy")
 
-    def filter(self, eps: float):
-        check(self.lib.bt_filter(self.h, eps), "filter")
+    def filter(self, eps: float, band: float = 1e-12) -> dict:
+        """Post-filter: drops blocks with ||C_ij||_F < eps.  Returns
+        {"dropped": n, "borderline": n} -- borderline blocks have
+        | ||C_ij|| - eps | <= band * eps."""
+        d, b = C.c_int64(), C.c_int64()
+        check(self.lib.bt_filter_report(self.h, eps, band, C.byref(d), C.byref(b)), "filter")
+        return {"dropped": d.value, "borderline": b.value}
 
 
 def multiply_local(ctx: Context, a: LocalStore, b: LocalStore, c: LocalStore,

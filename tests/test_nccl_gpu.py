@@ -31,3 +31,17 @@ def test_nccl_drivers(world, force_miss):
     print(p.stdout[-4000:])
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert p.stdout.count(": OK") >= 6
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c3_case1_vs_oracle(world):
+    """BASELINE c3 (10 %) through case 1 on `world` GPUs against the oracle."""
+    if _ngpu() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29600 + world), os.path.join(HERE, "c3_case1_worker.py"), "--occ", "0.10"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(p.stdout[-4000:])
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert ": OK" in p.stdout or "] OK" in p.stdout
