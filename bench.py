@@ -385,53 +385,55 @@ def main():
     alg_bytes = 8.0 * (av.size + bv.size * world + c_el) + 12.0 * (len(abi) + len(bbi) * world)
     achieved = flops_step / (kn_ms * 1e-3) / 1e12
 
-    # ---- e2e through the public API with host buffers (rank-local)
-    e2e_times = []
-    e2e_split = []   # debug: (put, multiply, export) ms per step, N > 1
-    cout = torch.empty(NB * NB * bsize, dtype=torch.float64).pin_memory()
+    # ---- e2e through the public API with host buffers (rank-local).  Every
+    # step uploads A and B from pinned host memory (put_blocks), multiplies and
+    # reads all of C back (export).  The C read-back is bt_mat_export_async:
+    # its D2H runs on a side stream while the next step's uploads and
+    # multiply proceed (PCIe is full duplex), so the steady state is bounded
+    # by the 667 MB C transfer per step.  Timed over the K steps as a whole,
+    # from a synchronised start to the last transfer landing (ctx.sync()).
+    couts = [torch.empty(NB * NB * bsize, dtype=torch.float64).pin_memory() for _ in range(2)]
     h2d = av.nbytes + bv.nbytes + 16 * (len(abi) + len(bbi))
     d2h = 0
-    for s in range(args.warmup + args.steps):
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
+
+    if world == 1:   # the user's stores, refilled every step (clear keeps capacity)
+        ea, eb, ec = LocalStore(ctx, sz, sz), LocalStore(ctx, sz, sz), LocalStore(ctx, sz, sz)
+
+    def e2e_step(s):
+        nonlocal d2h
         if world == 1:
-            ea = LocalStore(ctx, sz, sz)
-            ea.put_blocks(abi, abj, av_pin)
-            eb = LocalStore(ctx, sz, sz)
-            eb.put_blocks(bbi, bbj, bv_pin)
-            ec = LocalStore(ctx, sz, sz)
-            multiply_local(ctx, ea, eb, ec)
-            ci, cj, _ = ec.export(cout)
-            ctx.sync()
-            dt = time.perf_counter() - t0
-            d2h = 8 * int(ec.info()[1]) + 16 * len(ci)
             for x in (ea, eb, ec):
-                x.close()
+                x.clear()
+            ea.put_blocks(abi, abj, av_pin)
+            eb.put_blocks(bbi, bbj, bv_pin)
+            multiply_local(ctx, ea, eb, ec)
+            ci, cj, _ = ec.export(couts[s % 2], asynchronous=True)
+            d2h = 8 * int(ec.info()[1]) + 16 * len(ci)
         else:
             a.local(rank).clear()
             b.local(rank).clear()
             c.local(rank).clear()
             a.local(rank).put_blocks(abi + NB * rank, abj, av_pin)
             b.local(rank).put_blocks(bbi, bbj, bv_pin)
-            t1 = time.perf_counter()
             dd.multiply_virtual_case2(comm, a, b, c, world, gather=True)
-            t2 = time.perf_counter()
-            ci, cj, _ = c.local(rank).export(cout)
-            ctx.sync()
-            dt = time.perf_counter() - t0
-            if os.environ.get("BT_BENCH_DEBUG"):
-                e2e_split.append((round(1e3 * (t1 - t0), 2), round(1e3 * (t2 - t1), 2),
-                                  round(1e3 * (dt - (t2 - t0)), 2)))
+            ci, cj, _ = c.local(rank).export(couts[s % 2], asynchronous=True)
             d2h = 8 * int(c.local(rank).info()[1]) + 16 * len(ci)
-        if s >= args.warmup:
-            e2e_times.append(dt)
-    if os.environ.get("BT_BENCH_DEBUG"):
-        print(f"[rank {rank}] e2e_ms {np.round(np.array(e2e_times) * 1e3, 2).tolist()} "
-              f"split(put,mult,export) {e2e_split}", file=sys.stderr, flush=True)
+
+    for s in range(args.warmup):
+        e2e_step(s)
+    ctx.sync()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        e2e_step(s)
+    ctx.sync()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if world == 1:
+        for x in (ea, eb, ec):
+            x.close()
     gc.enable()
-    e2e_s = float(np.mean(e2e_times))
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -439,7 +441,7 @@ def main():
     e2e_val = flops_step * world / e2e_s / 1e9
 
     # ---- parity of this run's own C (rank 0's slab) against the reference
-    ref_out = None
+    ref_out, cb = None, None
     if rank == 0 and not args.no_cpu_baseline and world == 1:   # rank 0 at N = 1 only
         cb, ref_out = cpu_baseline_sample()
     elif rank == 0 and not args.no_parity:
@@ -486,7 +488,7 @@ def main():
         }
         if parity is not None:
             line["parity"] = parity
-        if world == 1 and ref_out is not None:
+        if cb is not None:
             line["cpu_baseline"] = cb
     if world > 1:
         comm.close()

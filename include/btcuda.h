@@ -74,6 +74,7 @@ int bt_version(void);
 int bt_get_unique_id(void* id128);
 int bt_ctx_create(int device, int nranks, int rank, const void* nccl_id, bt_ctx** out);
 int bt_ctx_destroy(bt_ctx* ctx);
+/* waits for all device work of the context (incl. asynchronous exports) */
 int bt_ctx_sync(bt_ctx* ctx);
 int bt_ctx_rank(const bt_ctx* ctx, int* rank, int* nranks);
 /* the context's CUDA stream (cudaStream_t), for callers that time with events */
@@ -106,6 +107,12 @@ int bt_mat_info(const bt_mat* m, int64_t* nblk, int64_t* nelems);
 /* Canonical (i, j)-sorted export of all stored blocks into host buffers of
  * nblk / nelems entries (bi, bj may be NULL to skip the index). */
 int bt_mat_export(const bt_mat* m, int64_t* bi, int64_t* bj, double* vals);
+/* bt_mat_export whose value transfer completes asynchronously: returns once
+ * bi/bj are filled and the D2H of the values into `vals` is enqueued on a side
+ * stream (the context's main stream stays free, so the next call's uploads and
+ * kernels overlap the transfer).  `vals` must stay valid, and must not be read,
+ * until bt_ctx_sync(ctx) returns.  Pinned `vals` give full PCIe speed. */
+int bt_mat_export_async(const bt_mat* m, int64_t* bi, int64_t* bj, double* vals);
 /* DistMatrix::get_block (matrix.hpp:323-325): copies block (i, j) into out
  * (rows*cols doubles); *found = 0 when it is not stored. */
 int bt_mat_get_block(const bt_mat* m, int64_t i, int64_t j, double* out, int* found);

@@ -86,6 +86,7 @@ SIGNATURES = {
     "bt_mat_put_blocks": (C.c_int, [C.c_void_p, C.c_int64, _i64p, _i64p, _f64p, C.c_int]),
     "bt_mat_info": (C.c_int, [C.c_void_p, _i64p, _i64p]),
     "bt_mat_export": (C.c_int, [C.c_void_p, _i64p, _i64p, _f64p]),
+    "bt_mat_export_async": (C.c_int, [C.c_void_p, _i64p, _i64p, _f64p]),
     "bt_mat_get_block": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, _f64p,
                                    C.POINTER(C.c_int)]),
     "bt_mat_norms": (C.c_int, [C.c_void_p, _f64p]),

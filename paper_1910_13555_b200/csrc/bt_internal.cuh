@@ -104,10 +104,15 @@ struct Ctx {
   void* nccl = nullptr; // ncclComm_t when nranks > 1
   DBuf<unsigned char> scratch;  // CUB temp storage, reused
   void* pinned = nullptr;       // small pinned host staging for scalar readbacks
+  // device alias of `pinned` (mapped page-locked memory): kernels write small
+  // results there directly, so reading them back needs no copy-engine D2H --
+  // which would queue behind an asynchronous export's bulk transfer
+  void* pinned_dev = nullptr;
   // Grow-only pinned host staging for index uploads: one packed H2D per call
   // instead of several pageable copies.  stage_ev marks the last copy that read
   // it; host_stage() waits for it before handing the buffer out again.
   unsigned char* hstage = nullptr;
+  unsigned char* hstage_dev = nullptr;  // device alias of hstage (mapped)
   size_t hstage_cap = 0;
   cudaEvent_t stage_ev = nullptr;
   unsigned char* host_stage(size_t bytes);
@@ -117,6 +122,15 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_join[kAux] = {};
   cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  // Export staging (T8 -> compact values, then D2H on aux[0]): two buffers
+  // used alternately; xfer_done[b] marks the last D2H that read buffer b, so a
+  // later export compacts into b only after it (asynchronous exports,
+  // bt_mat_export_async, leave the main stream free meanwhile).
+  DBuf<double> xstage[2];
+  cudaEvent_t xfer_done[2] = {nullptr, nullptr};
+  int xnext = 0;
+  // waits for every stream of the context (main + side streams)
+  void sync_all();
   void* ensure_scratch(size_t bytes);
   // Grow-only per-slot workspace for call-local temporaries (no allocator calls
   // in steady state).  Valid until the next use of the same slot.

@@ -991,7 +991,10 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     int64_t* val_base = x.ws<int64_t>(4, M + 1);
     unsigned long long* tot = x.ws<unsigned long long>(5, 3 + NSEG);
     BT_CUDA(cudaMemsetAsync(tot, 0, sizeof(unsigned long long) * (3 + NSEG), st));
-    unsigned long long* dsizes = x.ws<unsigned long long>(11, 6 + NSEG);
+    // sizes for the host: written by the scan kernel straight into mapped
+    // page-locked memory (a copy-engine D2H would queue behind an
+    // asynchronous export's transfer)
+    unsigned long long* dsizes = reinterpret_cast<unsigned long long*>(x.pinned_dev);
     unsigned long long* cursor = x.ws<unsigned long long>(18, NSEG + NCLASS);
     ra.row_nnz = row_nnz;
     ra.row_prod = row_prod;
@@ -1028,8 +1031,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       unsigned long long tot[3 + NSEG];
     };
     static_assert(sizeof(Sizes) <= 2048, "pinned staging");
-    Sizes& h = *reinterpret_cast<Sizes*>(x.pinned);  // pinned: one readback
-    BT_CUDA(cudaMemcpyAsync(&h, dsizes, sizeof(Sizes), cudaMemcpyDeviceToHost, st));
+    // the scan kernel wrote the sizes into mapped pinned memory (no D2H copy)
+    Sizes& h = *reinterpret_cast<Sizes*>(x.pinned);
     const bool phases = x.timing && env_int("BT_PHASES", 0);
     if (phases) BT_CUDA(cudaEventRecord(x.ev[4], st));
     tr.mark("pass1 enqueued");

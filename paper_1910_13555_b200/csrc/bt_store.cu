@@ -56,13 +56,20 @@ void* Ctx::ensure_scratch(size_t bytes) {
   return scratch.p;
 }
 
+void Ctx::sync_all() {
+  BT_CUDA(cudaStreamSynchronize(stream));
+  for (auto& a : aux)
+    if (a) BT_CUDA(cudaStreamSynchronize(a));
+}
+
 unsigned char* Ctx::host_stage(size_t bytes) {
   BT_CUDA(cudaEventSynchronize(stage_ev));  // the previous upload has read it
   if (hstage_cap < bytes) {
     if (hstage) BT_CUDA(cudaFreeHost(hstage));
     hstage = nullptr;
     const size_t cap = std::max(bytes + bytes / 4, size_t(1) << 20);
-    BT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hstage), cap, cudaHostAllocDefault));
+    BT_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hstage), cap, cudaHostAllocMapped));
+    BT_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hstage_dev), hstage, 0));
     hstage_cap = cap;
   }
   return hstage;
@@ -215,6 +222,22 @@ __global__ void k_export_plan(const int32_t* __restrict__ row_ptr, const int32_t
   bi[e] = lo;
   bj[e] = j;
   len[e] = static_cast<int64_t>(rsz[lo]) * csz[j];
+}
+
+// Export metadata straight into mapped page-locked host memory (no copy-engine
+// D2H, which would queue behind a pending asynchronous value transfer): the
+// block index (bi, bj) of every entry, and the compact offsets of the chunk
+// boundaries the host needs to enqueue the per-chunk value copies.
+__global__ void k_export_meta(const int64_t* __restrict__ d_bi, const int64_t* __restrict__ d_bj,
+                              const int64_t* __restrict__ coff, int64_t n,
+                              int64_t* __restrict__ h_bi, int64_t* __restrict__ h_bj,
+                              const int64_t* __restrict__ cb, int ncb, int64_t* __restrict__ h_co) {
+  const int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (h_bi && e < n) {
+    h_bi[e] = d_bi[e];
+    h_bj[e] = d_bj[e];
+  }
+  if (e < ncb) h_co[e] = coff[cb[e]];
 }
 
 // T8 slot -> compact row-major (host order).  dst may be mapped host memory:
@@ -446,11 +469,13 @@ int bt_ctx_create(int device, int nranks, int rank, const void* nccl_id, bt_ctx*
     BT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t thr = UINT64_MAX;
     BT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    BT_CUDA(cudaMallocHost(&x.pinned, 4096));
+    BT_CUDA(cudaHostAlloc(&x.pinned, 4096, cudaHostAllocMapped));
+    BT_CUDA(cudaHostGetDevicePointer(&x.pinned_dev, x.pinned, 0));
     BT_CUDA(cudaEventCreateWithFlags(&x.stage_ev, cudaEventDisableTiming));
     for (auto& e : x.ev) BT_CUDA(cudaEventCreate(&e));
     for (auto& a : x.aux) BT_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
     BT_CUDA(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming));
+    for (auto& e : x.xfer_done) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : x.ev_join) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (nranks > 1) {
       ncclUniqueId id;
@@ -474,6 +499,11 @@ int bt_ctx_destroy(bt_ctx* c) {
     Ctx& x = c->impl;
     cudaSetDevice(x.device);
     cudaStreamSynchronize(x.stream);
+    for (auto& a : x.aux)
+      if (a) cudaStreamSynchronize(a);  // asynchronous exports still in flight
+    for (auto& b : x.xstage) b.release();
+    for (auto& e : x.xfer_done)
+      if (e) cudaEventDestroy(e);
     x.scratch.release();
     for (auto& w : x.ws_slots) w.release();
     cudaStreamSynchronize(x.stream);
@@ -496,7 +526,7 @@ int bt_ctx_destroy(bt_ctx* c) {
 int bt_ctx_sync(bt_ctx* c) {
   return guard([&] {
     BT_REQUIRE(c, BT_ERR_INVALID_ARGUMENT, "null context");
-    BT_CUDA(cudaStreamSynchronize(c->impl.stream));
+    c->impl.sync_all();
   });
 }
 
@@ -635,7 +665,13 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
       in_total += int64_t(m.h_rsz[bi[t]]) * m.h_csz[bj[t]];
     }
     tr.mark("validate");
-    HostIndex old = download_index(m);
+    // an empty store's index is known on the host (no D2H: a copy-engine
+    // readback would queue behind an asynchronous export's transfer)
+    HostIndex old;
+    if (m.nblk == 0)
+      old.row_ptr.assign(m.nbr + 1, 0);
+    else
+      old = download_index(m);
     tr.mark("download_index");
     // values first, so the copy runs while the host plans the merge.
     // device: inputs already in this GPU's memory or in mapped page-locked host
@@ -719,7 +755,13 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
                "store exceeds 2^31 blocks");
     tr.mark("plan");
     const int64_t nout = static_cast<int64_t>(col.size());
-    DBuf<double> new_vals(std::max<int64_t>(nv, 2), st);
+    // an empty store (bt_mat_clear keeps its slab as capacity) is refilled in
+    // place: a clear + put cycle allocates nothing
+    DBuf<double> new_vals;
+    if (m.nblk == 0 && m.vals.n >= static_cast<size_t>(std::max<int64_t>(nv, 2)))
+      new_vals = std::move(m.vals);
+    else
+      new_vals.alloc(std::max<int64_t>(nv, 2), st);
     BT_CUDA(cudaMemsetAsync(new_vals.p, 0, sizeof(double) * std::max<int64_t>(nv, 2), st));
     tr.mark("slab_alloc");
     // plan arrays: one device buffer, one packed upload through the pinned stage
@@ -747,10 +789,24 @@ int bt_mat_put_blocks(bt_mat* mh, int64_t n, const int64_t* bi, const int64_t* b
   });
 }
 
+static void export_store(const Mat& m, int64_t* bi, int64_t* bj, double* vals, bool async);
+
 int bt_mat_export(const bt_mat* mh, int64_t* bi, int64_t* bj, double* vals) {
   return guard([&] {
     check_mat(mh);
-    const Mat& m = mh->impl;
+    export_store(mh->impl, bi, bj, vals, false);
+  });
+}
+
+int bt_mat_export_async(const bt_mat* mh, int64_t* bi, int64_t* bj, double* vals) {
+  return guard([&] {
+    check_mat(mh);
+    export_store(mh->impl, bi, bj, vals, true);
+  });
+}
+
+static void export_store(const Mat& m, int64_t* bi, int64_t* bj, double* vals, bool async) {
+  {
     Ctx& x = *m.ctx;
     BT_CUDA(cudaSetDevice(x.device));
     if (m.nblk == 0) return;
@@ -773,6 +829,30 @@ int bt_mat_export(const bt_mat* mh, int64_t* bi, int64_t* bj, double* vals) {
     cub::DeviceScan::ExclusiveSum(tmp, bytes, d_coff, d_coff, n + 1, st);
     check_launch("export_scan");
     count_launch(&x);
+    // index + chunk offsets into mapped host memory, then one sync of the
+    // main stream (which holds no pending value transfer)
+    constexpr int kChunks = 8;
+    int64_t cb[kChunks + 1];
+    for (int c = 0; c <= kChunks; ++c) cb[c] = n * c / kChunks;
+    unsigned char* hs = nullptr;
+    unsigned char* hs_dev = nullptr;
+    if (bi || bj) {
+      hs = x.host_stage(2 * sizeof(int64_t) * n);
+      hs_dev = x.hstage_dev;
+    }
+    int64_t* d_cb = x.ws<int64_t>(22, kChunks + 1);
+    BT_CUDA(cudaMemcpyAsync(d_cb, cb, sizeof(cb), cudaMemcpyHostToDevice, st));
+    int64_t* meta_co = reinterpret_cast<int64_t*>(x.pinned);
+    k_export_meta<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+        d_bi, d_bj, d_coff, n, reinterpret_cast<int64_t*>(hs_dev),
+        hs_dev ? reinterpret_cast<int64_t*>(hs_dev) + n : nullptr, d_cb, kChunks + 1,
+        reinterpret_cast<int64_t*>(x.pinned_dev));
+    check_launch("export_meta");
+    count_launch(&x);
+    BT_CUDA(cudaEventRecord(x.stage_ev, st));
+    BT_CUDA(cudaStreamSynchronize(st));
+    if (bi) std::memcpy(bi, hs, sizeof(int64_t) * n);
+    if (bj) std::memcpy(bj, hs + sizeof(int64_t) * n, sizeof(int64_t) * n);
     tr.mark("plan");
     if (vals) {
       double* alias = zero_copy_enabled() ? static_cast<double*>(mapped_host_alias(vals)) : nullptr;
@@ -783,19 +863,18 @@ int bt_mat_export(const bt_mat* mh, int64_t* bi, int64_t* bj, double* vals) {
         check_launch("compact");
         count_launch(&x);
       } else {
-        // compact in chunks on the main stream; each chunk's D2H runs on a side
-        // stream as soon as it is compacted (the transfer hides the compaction)
-        double* dst = x.ws<double>(27, m.nelems);
-        int64_t* hco = reinterpret_cast<int64_t*>(x.pinned);  // chunk boundaries' offsets
-        constexpr int kChunks = 8;
-        int64_t cb[kChunks + 1];
-        for (int c = 0; c <= kChunks; ++c) cb[c] = n * c / kChunks;
-        for (int c = 0; c <= kChunks; ++c)
-          BT_CUDA(cudaMemcpyAsync(hco + c, d_coff + cb[c], sizeof(int64_t), cudaMemcpyDeviceToHost,
-                                  st));
-        BT_CUDA(cudaStreamSynchronize(st));
+        // compact in chunks on the main stream into a staging buffer; each
+        // chunk's D2H runs on a side stream as soon as it is compacted (the
+        // transfer hides the compaction).  Two staging buffers alternate: this
+        // export's compaction waits only for the D2H that last read its buffer.
+        const int xb = x.xnext;
+        x.xnext ^= 1;
+        BT_CUDA(cudaStreamWaitEvent(st, x.xfer_done[xb], 0));
+        if (x.xstage[xb].n < static_cast<size_t>(std::max<int64_t>(m.nelems, 1)))
+          x.xstage[xb].alloc(std::max<int64_t>(m.nelems, 1) + m.nelems / 4, st);
+        double* dst = x.xstage[xb].p;
         int64_t eo[kChunks + 1];
-        for (int c = 0; c <= kChunks; ++c) eo[c] = hco[c];
+        for (int c = 0; c <= kChunks; ++c) eo[c] = meta_co[c];
         cudaStream_t cs = x.aux[0];
         for (int c = 0; c < kChunks; ++c) {
           if (cb[c + 1] == cb[c]) continue;
@@ -808,25 +887,15 @@ int bt_mat_export(const bt_mat* mh, int64_t* bi, int64_t* bj, double* vals) {
           BT_CUDA(cudaMemcpyAsync(vals + eo[c], dst + eo[c], sizeof(double) * (eo[c + 1] - eo[c]),
                                   cudaMemcpyDeviceToHost, cs));
         }
-        BT_CUDA(cudaEventRecord(x.ev_fork, cs));
-        BT_CUDA(cudaStreamWaitEvent(st, x.ev_fork, 0));
+        BT_CUDA(cudaEventRecord(x.xfer_done[xb], cs));
+        // synchronous export: the values are in `vals` when the call returns
+        if (!async) BT_CUDA(cudaStreamWaitEvent(st, x.xfer_done[xb], 0));
       }
       tr.mark("compact_enqueue");
     }
-    // block indices through the pinned stage
-    if (bi || bj) {
-      unsigned char* hs = x.host_stage(2 * sizeof(int64_t) * n);
-      BT_CUDA(cudaMemcpyAsync(hs, d_bi, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
-      BT_CUDA(cudaMemcpyAsync(hs + sizeof(int64_t) * n, d_bj, sizeof(int64_t) * n,
-                              cudaMemcpyDeviceToHost, st));
-      BT_CUDA(cudaEventRecord(x.stage_ev, st));
-      BT_CUDA(cudaStreamSynchronize(st));
-      if (bi) std::memcpy(bi, hs, sizeof(int64_t) * n);
-      if (bj) std::memcpy(bj, hs + sizeof(int64_t) * n, sizeof(int64_t) * n);
-    }
-    BT_CUDA(cudaStreamSynchronize(st));
+    if (!async) BT_CUDA(cudaStreamSynchronize(st));
     tr.mark("d2h");
-  });
+  }
 }
 
 int bt_mat_get_block(const bt_mat* mh, int64_t i, int64_t j, double* out, int* found) {

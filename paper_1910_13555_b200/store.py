@@ -140,8 +140,10 @@ class LocalStore:
     def nblk(self) -> int:
         return self.info()[0]
 
-    def export(self, vals_out=None):
-        """Canonical (bi, bj, vals) -- vals may be a preallocated (pinned) buffer."""
+    def export(self, vals_out=None, asynchronous: bool = False):
+        """Canonical (bi, bj, vals) -- vals may be a preallocated (pinned) buffer.
+        asynchronous=True (bt_mat_export_async): returns once bi/bj are filled;
+        the values land in `vals` by the next Context.sync()."""
         nb, ne = self.info()
         bi = np.zeros(nb, np.int64)
         bj = np.zeros(nb, np.int64)
@@ -151,7 +153,8 @@ class LocalStore:
         else:
             vals = vals_out
             vp = C.cast(C.c_void_p(vals_out.data_ptr()), _f64p)
-        check(self.lib.bt_mat_export(self.h, ptr(bi, _i64p), ptr(bj, _i64p), vp), "export")
+        fn = self.lib.bt_mat_export_async if asynchronous else self.lib.bt_mat_export
+        check(fn(self.h, ptr(bi, _i64p), ptr(bj, _i64p), vp), "export")
         return bi, bj, vals
 
     def get_block(self, i: int, j: int):

@@ -246,6 +246,38 @@ def test_export_to_pinned_and_pageable(oracle, ctx):
     s.close()
 
 
+def test_export_async_overlaps_next_multiply(oracle, ctx):
+    """bt_mat_export_async: the value transfer runs on a side stream while the
+    next calls (puts, a multiply into a new C, another async export, a sync
+    export) proceed; after ctx.sync() every buffer holds its store exactly."""
+    import torch
+    from oracle.oracle import Blocks
+    from paper_1910_13555_b200.store import LocalStore, multiply_local
+    sz = np.array([5, 13, 23], np.int32)[np.random.default_rng(9).integers(0, 3, 120)]
+    A = oracle.random_matrix(811, sz, sz, 0.2)
+    B = oracle.random_matrix(812, sz, sz, 0.2)
+    want1, _, _ = oracle.multiply(A, B, Blocks.empty(sz, sz))
+    want2, _, _ = oracle.multiply(B, A, Blocks.empty(sz, sz))
+    a, b = to_store(ctx, A), to_store(ctx, B)
+    outs, wants = [], []
+    for it in range(3):
+        for (x, y, w) in ((a, b, want1), (b, a, want2)):
+            c = LocalStore(ctx, sz, sz)
+            multiply_local(ctx, x, y, c)
+            buf = torch.full((len(w.vals),), np.nan, dtype=torch.float64).pin_memory()
+            bi, bj, _ = c.export(buf, asynchronous=True)
+            assert np.array_equal(bi, w.bi) and np.array_equal(bj, w.bj)
+            outs.append(buf)
+            wants.append(w)
+            c.close()   # the staged values outlive the store
+    # a synchronous export in between still returns complete values
+    got = from_store(a)
+    assert np.array_equal(got.vals, A.vals)
+    ctx.sync()
+    for buf, w in zip(outs, wants):
+        assert_parity(Blocks(w.rsz, w.csz, w.bi, w.bj, buf.numpy()), w)
+
+
 @pytest.mark.parametrize("case", ["empty_a", "empty_b", "empty_all", "disjoint_k", "zero_blocks",
                                   "single_1x1", "eps_filters_all"])
 def test_edge_cases(oracle, ctx, case):
