@@ -72,6 +72,10 @@ struct RowArgs {
   int sort_min;   // rows with more A entries per chunk emit by window sort
   bool colmask;   // k_row_fill has a 64-bit per-column mask array (N <= kMaskCols)
   int tall_rows;  // tile height for blocks taller than 32 rows (24 or 32)
+  // column chunk width of the symbolic passes: rows are processed in chunks
+  // of `colw` block columns (per-column counters in shared memory are sized
+  // for one chunk), so C may have any number of block columns
+  int64_t colw;
   int splits;     // k_row_fill CTAs per C row (long rows: chunk ranges)
   bool dmma_ok;
   // pass 1 outputs
@@ -117,8 +121,21 @@ struct RowChunk {  // shared-memory staging of up to kChunkA A entries
   int32_t au[kChunkA];   // T8 tile offset of the A block (offset / 64)
 };
 
-// Stage A entries [e0, e0 + kChunkA) of row i; returns the pair count of the chunk.
-__device__ int64_t stage_chunk(const RowArgs& g, int32_t e0, int32_t e1, RowChunk& rc) {
+// first position in b_col[lo, hi) with column >= j (B rows are column sorted)
+__device__ __forceinline__ int32_t col_lower_bound(const int32_t* __restrict__ col, int32_t lo,
+                                                   int32_t hi, int64_t j) {
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (col[mid] < j) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Stage A entries [e0, e0 + kChunkA) of row i; returns the pair count of the
+// chunk.  Pairs are restricted to C columns [j0, j1) (the current column chunk;
+// the whole row when [0, ncols)).
+__device__ int64_t stage_chunk(const RowArgs& g, int32_t e0, int32_t e1, RowChunk& rc,
+                               int64_t j0, int64_t j1) {
   using BS = cub::BlockScan<int32_t, kChunkA>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int32_t total;
@@ -126,8 +143,10 @@ __device__ int64_t stage_chunk(const RowArgs& g, int32_t e0, int32_t e1, RowChun
   int32_t len = 0;
   if (e < e1) {
     const int32_t k = g.a_col[e];
-    const int32_t b0 = g.b_rp[k];
-    len = g.b_rp[k + 1] - b0;
+    int32_t b0 = g.b_rp[k], b1 = g.b_rp[k + 1];
+    if (j0 > 0) b0 = col_lower_bound(g.b_col, b0, b1, j0);
+    if (j1 < g.ncols) b1 = col_lower_bound(g.b_col, b0, b1, j1);
+    len = b1 - b0;
     rc.k[threadIdx.x] = k;
     rc.b0[threadIdx.x] = b0;
     // per-entry constants the emission loops need, loaded once here (in
@@ -165,18 +184,21 @@ __device__ __forceinline__ int find_entry(const RowChunk& rc, int n, int32_t t) 
 // loads; returns whether the cache is valid.
 // before / split_c0 (split fill CTAs): before[j] also counts the kept pairs of
 // the A entries ahead of split_c0 (the chunks of the earlier CTAs of the row).
+// Counters are local to the column chunk [j0, j0 + jw): cnt[j - j0].
 __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_t* bits,
                              RowChunk& rc, unsigned long long* cand, unsigned long long* mnk,
+                             int64_t j0, int64_t jw,
                              uint32_t* cache_j = nullptr, int32_t* cache_bu = nullptr,
                              uint32_t* before = nullptr, int32_t split_c0 = 0) {
-  const int nw = static_cast<int>((g.ncols + 31) >> 5);
-  for (int64_t j = threadIdx.x; j < g.ncols; j += blockDim.x) cnt[j] = 0u;
+  const int nw = static_cast<int>((jw + 31) >> 5);
+  for (int64_t j = threadIdx.x; j < jw; j += blockDim.x) cnt[j] = 0u;
   if (before)
-    for (int64_t j = threadIdx.x; j < g.ncols; j += blockDim.x) before[j] = 0u;
+    for (int64_t j = threadIdx.x; j < jw; j += blockDim.x) before[j] = 0u;
   for (int w = threadIdx.x; w < nw; w += blockDim.x) bits[w] = 0u;
   __syncthreads();
   for (int32_t e = g.c_rp[i] + threadIdx.x; e < g.c_rp[i + 1]; e += blockDim.x) {
-    const int32_t j = g.c_col[e];
+    const int64_t j = g.c_col[e] - j0;
+    if (j < 0 || j >= jw) continue;
     cnt[j] = kCinFlag;
     atomicOr(&bits[j >> 5], 1u << (j & 31));
   }
@@ -184,7 +206,7 @@ __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
   bool cached = false;
   for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
     const int n = min(kChunkA, a1 - c0);
-    const int64_t T = stage_chunk(g, c0, a1, rc);
+    const int64_t T = stage_chunk(g, c0, a1, rc, j0, j0 + jw);
     const bool cache = cache_j && a1 - a0 <= kChunkA && T <= kPairCap;
     const bool ahead = before && c0 < split_c0;
     for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
@@ -195,14 +217,14 @@ __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
         if (cache) cache_j[t] = 0xffffffffu;
         continue;
       }
-      const int32_t j = g.b_col[f];
+      const int32_t j = static_cast<int32_t>(g.b_col[f] - j0);
       if (cache) {
         cache_j[t] = static_cast<uint32_t>(j);
         cache_bu[t] = static_cast<int32_t>(g.b_off[f] >> 6);
       }
       if (atomicAdd(&cnt[j], 1u) == 0u) atomicOr(&bits[j >> 5], 1u << (j & 31));
       if (ahead) atomicAdd(&before[j], 1u);
-      if (mnk) *mnk += static_cast<unsigned long long>(rc.ksz[l]) * g.n_sz[j];
+      if (mnk) *mnk += static_cast<unsigned long long>(rc.ksz[l]) * g.n_sz[j + j0];
     }
     __syncthreads();
     cached = cache;
@@ -251,29 +273,35 @@ __device__ int compact_touched(const uint32_t* bits, int nw, int32_t* tcol) {
 // stored elements, per-class work items, useful flops.
 __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
   extern __shared__ uint32_t cnt[];
-  uint32_t* bits = cnt + g.ncols;
-  int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.ncols + 31) >> 5));
+  uint32_t* bits = cnt + g.colw;
+  int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.colw + 31) >> 5));
   __shared__ unsigned long long cls_items[NSEG];
   __shared__ RowChunk rc;
   const int64_t i = blockIdx.x;
   for (int t = threadIdx.x; t < NSEG; t += blockDim.x) cls_items[t] = 0;
   unsigned long long cand = 0, mnk = 0;
-  row_products(g, i, cnt, bits, rc, &cand, &mnk);
   const int m = g.m_sz[i];
   long long nnz = 0, prods = 0, vals = 0, elems = 0;
-  const int ntouch = compact_touched(bits, static_cast<int>((g.ncols + 31) >> 5), tcol);
-  for (int q = threadIdx.x; q < ntouch; q += blockDim.x) {
-    const int j = tcol[q];
-    const uint32_t v = cnt[j];
-    const int n = g.n_sz[j];
-    ++nnz;
-    prods += v & ~kCinFlag;
-    vals += t8_size(m, n);
-    elems += static_cast<long long>(m) * n;
-    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
-    const int seg = cls * kMaxBands + band_of(j, g);
-    agg_add(&cls_items[seg], seg,
-            static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
+  // column chunks (one when the row fits the shared-memory counters)
+  for (int64_t j0 = 0; j0 < g.ncols; j0 += g.colw) {
+    const int64_t jw = min(g.colw, g.ncols - j0);
+    row_products(g, i, cnt, bits, rc, &cand, &mnk, j0, jw);
+    const int ntouch = compact_touched(bits, static_cast<int>((jw + 31) >> 5), tcol);
+    for (int q = threadIdx.x; q < ntouch; q += blockDim.x) {
+      const int jl = tcol[q];
+      const int64_t j = j0 + jl;
+      const uint32_t v = cnt[jl];
+      const int n = g.n_sz[j];
+      ++nnz;
+      prods += v & ~kCinFlag;
+      vals += t8_size(m, n);
+      elems += static_cast<long long>(m) * n;
+      const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
+      const int seg = cls * kMaxBands + band_of(j, g);
+      agg_add(&cls_items[seg], seg,
+              static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
+    }
+    __syncthreads();  // counters are cleared for the next chunk
   }
   // the six row sums in one reduction: shuffles within each warp, one
   // barrier, then thread 0 adds the per-warp partials (exact integer sums)
@@ -320,8 +348,8 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
 __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                                        // counts -> C entry rank
-  int32_t* cur = reinterpret_cast<int32_t*>(sm + g.ncols);  // product cursor
-  uint32_t* bits = sm + 2 * g.ncols;                         // touched columns
+  int32_t* cur = reinterpret_cast<int32_t*>(sm + g.colw);  // product cursor
+  uint32_t* bits = sm + 2 * g.colw;                         // touched columns
   __shared__ RowChunk rc;
   __shared__ int32_t s_bu[kPairCap];  // B tile offset of staged pair
   __shared__ int16_t s_l[kPairCap];   // local A entry of staged pair
@@ -343,18 +371,24 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   const int32_t e_hi = min(a1, a0 + ch_hi * kChunkA);
   uint32_t* before = nullptr;
   if (split > 0)
-    before = sm + (g.colmask ? ((3 * g.ncols + ((g.ncols + 31) >> 5) + 1) & ~int64_t(1)) +
-                                   2 * g.ncols
-                             : 3 * g.ncols + ((g.ncols + 31) >> 5));
+    before = sm + (g.colmask ? ((3 * g.colw + ((g.colw + 31) >> 5) + 1) & ~int64_t(1)) +
+                                   2 * g.colw
+                             : 3 * g.colw + ((g.colw + 31) >> 5));
   for (int t = threadIdx.x; t < NSEG; t += blockDim.x) cls_n[t] = 0;
-  // single-chunk rows: pair columns / B offsets cached, rc stays staged
-  const bool cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, s_key, s_bu, before,
-                                   e_lo);
   const int m = g.m_sz[i];
   const int32_t cbase = g.out_rp[i];
   const int64_t pbase = g.prod_base[i], vbase = g.val_base[i];
-  int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.ncols + 31) >> 5));
-  const int ntouch = compact_touched(bits, static_cast<int>((g.ncols + 31) >> 5), tcol);
+  int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.colw + 31) >> 5));
+  // C columns in chunks of colw (one chunk when the row fits the shared-memory
+  // counters): C entries, ranks and product cursors continue across chunks
+  long long run_prod = 0, run_val = 0;
+  int run_q = 0;
+  for (int64_t j0 = 0; j0 < g.ncols; j0 += g.colw) {
+  const int64_t jw = min(g.colw, g.ncols - j0);
+  // single-chunk rows: pair columns / B offsets cached, rc stays staged
+  const bool cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, j0, jw, s_key, s_bu,
+                                   before, e_lo);
+  const int ntouch = compact_touched(bits, static_cast<int>((jw + 31) >> 5), tcol);
   {
     // touched columns in ascending order, 256 at a time: ranks, product bases
     // and T8 offsets by block scans
@@ -364,13 +398,13 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
     constexpr int kW = kChunkA / 32;
     __shared__ long long wt[2][kW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    long long run_prod = 0, run_val = 0;
     for (int q0 = 0; q0 < ntouch; q0 += blockDim.x) {
       const int q = q0 + threadIdx.x;
       const bool ok = q < ntouch;
-      const int j = ok ? tcol[q] : 0;
+      const int j = ok ? tcol[q] : 0;  // chunk-local column
+      const int64_t jg = j0 + j;
       const uint32_t cj = ok ? cnt[j] : 0u;
-      const int n = ok ? g.n_sz[j] : 0;
+      const int n = ok ? g.n_sz[jg] : 0;
       const long long np = cj & ~kCinFlag, tv = ok ? t8_size(m, n) : 0;
       long long pi = np, vi = tv;
 #pragma unroll
@@ -401,17 +435,17 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       __syncthreads();
       if (ok && split > 0) cur[j] = static_cast<int32_t>(run_prod + p_ex + before[j]);
       if (ok && split == 0) {
-        const int32_t c = cbase + q;
-        g.out_col[c] = static_cast<int32_t>(j);
+        const int32_t c = cbase + run_q + q;
+        g.out_col[c] = static_cast<int32_t>(jg);
         g.out_row[c] = static_cast<int32_t>(i);
         g.out_off[c] = vbase + run_val + v_ex;
         g.cin_map[c] = -1;
         g.out_np[c] = static_cast<int32_t>(np);
         g.out_p0[c] = pbase + run_prod + p_ex;
         cur[j] = static_cast<int32_t>(run_prod + p_ex);
-        cnt[j] = static_cast<uint32_t>(q);
+        cnt[j] = static_cast<uint32_t>(run_q + q);  // rank of the C entry in the row
         const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
-        const int seg = cls * kMaxBands + band_of(j, g);
+        const int seg = cls * kMaxBands + band_of(jg, g);
         agg_add(&cls_n[seg], seg,
                 static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
       }
@@ -419,49 +453,22 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       run_val += v_tot;
     }
   }
+  run_q += ntouch;
   __syncthreads();
-  if (split == 0) {
-  // reserve this row's work items in every class segment (one atomic per class)
-  for (int t = threadIdx.x; t < NSEG; t += blockDim.x) {
-    const unsigned long long k = cls_n[t];
-    cls_at[t] = k ? atomicAdd(&g.class_cursor[t], k) : 0ull;
-  }
-  __syncthreads();
-  // C_in blocks: slot of the matching C_out block
-  for (int32_t e = g.c_rp[i] + threadIdx.x; e < g.c_rp[i + 1]; e += blockDim.x)
-    g.cin_map[cbase + cnt[g.c_col[e]]] = g.c_off[e];
-  __syncthreads();
-  // work items of this row: tall blocks become 32-row tiles
-  for (int32_t c = cbase + threadIdx.x; c < g.out_rp[i + 1]; c += blockDim.x) {
-    const int j = g.out_col[c];
-    const int n = g.n_sz[j];
-    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
-    const int nt = class_tiles(m, cls, g.tall_rows);
-    const int seg = cls * kMaxBands + band_of(j, g);
-    const unsigned long long at = agg_add(&cls_at[seg], seg, static_cast<unsigned long long>(nt));
-    const int64_t cin = g.cin_map[c];
-    const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
-    for (int q = 0; q < nt; ++q) {
-      const int r0 = g.tall_rows * q;
-      Item it;
-      it.c_off = g.out_off[c] + (r0 >> 3) * tile_row;
-      it.cin_off = cin >= 0 ? cin + (r0 >> 3) * tile_row : -1;
-      it.p0r8 = g.out_p0[c] | (static_cast<int64_t>(r0 >> 3) << 48);
-      it.np = g.out_np[c];
-      it.rows = static_cast<int16_t>(nt > 1 ? min(g.tall_rows, m - r0) : m);
-      it.n = static_cast<int16_t>(n);
-      g.items[at + q] = it;
+  // C_in blocks of this chunk: slot of the matching C_out block
+  if (split == 0)
+    for (int32_t e = g.c_rp[i] + threadIdx.x; e < g.c_rp[i + 1]; e += blockDim.x) {
+      const int64_t jl = g.c_col[e] - j0;
+      if (jl >= 0 && jl < jw) g.cin_map[cbase + cnt[jl]] = g.c_off[e];
     }
-  }
-  }  // split == 0
-  // products, k ascending (this CTA's chunks)
+  // ---- products of this column chunk, k ascending (this CTA's A chunks)
   for (int32_t c0 = e_lo; c0 < e_hi; c0 += kChunkA) {
     const int n = min(kChunkA, a1 - c0);
-    const int64_t T = cached ? rc.pref[n] : stage_chunk(g, c0, a1, rc);
+    const int64_t T = cached ? rc.pref[n] : stage_chunk(g, c0, a1, rc, j0, j0 + jw);
     if (cached && g.colmask && n <= 64) {
       // rank emission from the cached pairs (no global loads in the sweeps)
       unsigned long long* mask = reinterpret_cast<unsigned long long*>(
-          sm + ((3 * g.ncols + ((g.ncols + 31) >> 5) + 1) & ~int64_t(1)));
+          sm + ((3 * g.colw + ((g.colw + 31) >> 5) + 1) & ~int64_t(1)));
       for (int q = threadIdx.x; q < ntouch; q += blockDim.x) mask[tcol[q]] = 0ull;
       __syncthreads();
       for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
@@ -492,21 +499,21 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       // the number of lower entries l' < l in that column, i.e. k ascending,
       // in two parallel sweeps over the pairs -- no step per k.
       unsigned long long* mask = reinterpret_cast<unsigned long long*>(
-          sm + ((3 * g.ncols + ((g.ncols + 31) >> 5) + 1) & ~int64_t(1)));
+          sm + ((3 * g.colw + ((g.colw + 31) >> 5) + 1) & ~int64_t(1)));
       for (int q = threadIdx.x; q < ntouch; q += blockDim.x) mask[tcol[q]] = 0ull;
       __syncthreads();
       for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
         const int l = find_entry(rc, n, static_cast<int32_t>(t));
         const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
         if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
-        atomicOr(&mask[g.b_col[f]], 1ull << l);
+        atomicOr(&mask[g.b_col[f] - j0], 1ull << l);
       }
       __syncthreads();
       for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
         const int l = find_entry(rc, n, static_cast<int32_t>(t));
         const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
         if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
-        const int32_t j = g.b_col[f];
+        const int32_t j = static_cast<int32_t>(g.b_col[f] - j0);
         const int32_t p = cur[j] + __popcll(mask[j] & ((1ull << l) - 1ull));
         g.desc[pbase + p] = make_int4(rc.au[l], static_cast<int32_t>(g.b_off[f] >> 6),
                                       (rc.ksz[l] + 3) >> 2, rc.k[l]);
@@ -532,7 +539,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
           const int l = find_entry(rc, n, static_cast<int32_t>(t));
           const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
           const bool keep = keep_product(g.na, g.nb, c0 + l, f, g.eps);
-          s_key[slot] = keep ? static_cast<uint32_t>(g.b_col[f]) : 0xffffffffu;
+          s_key[slot] = keep ? static_cast<uint32_t>(g.b_col[f] - j0) : 0xffffffffu;
           s_bu[slot] = static_cast<int32_t>(g.b_off[f] >> 6);
         }
         __syncthreads();
@@ -566,7 +573,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
           const int l = find_entry(rc, n, static_cast<int32_t>(t));
           const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
           if (keep_product(g.na, g.nb, c0 + l, f, g.eps)) {
-            keys[u] = (static_cast<uint32_t>(g.b_col[f]) << 11) | static_cast<uint32_t>(slot);
+            keys[u] = (static_cast<uint32_t>(g.b_col[f] - j0) << 11) | static_cast<uint32_t>(slot);
             s_bu[slot] = static_cast<int32_t>(g.b_off[f] >> 6);
             s_l[slot] = static_cast<int16_t>(l);
           }
@@ -614,6 +621,38 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       __syncthreads();
     }
   }
+  __syncthreads();
+  }  // column chunks
+  if (split == 0) {
+  // reserve this row's work items in every class segment (one atomic per class)
+  for (int t = threadIdx.x; t < NSEG; t += blockDim.x) {
+    const unsigned long long k = cls_n[t];
+    cls_at[t] = k ? atomicAdd(&g.class_cursor[t], k) : 0ull;
+  }
+  __syncthreads();
+  // work items of this row: tall blocks become 32-row tiles
+  for (int32_t c = cbase + threadIdx.x; c < g.out_rp[i + 1]; c += blockDim.x) {
+    const int j = g.out_col[c];
+    const int n = g.n_sz[j];
+    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
+    const int nt = class_tiles(m, cls, g.tall_rows);
+    const int seg = cls * kMaxBands + band_of(j, g);
+    const unsigned long long at = agg_add(&cls_at[seg], seg, static_cast<unsigned long long>(nt));
+    const int64_t cin = g.cin_map[c];
+    const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
+    for (int q = 0; q < nt; ++q) {
+      const int r0 = g.tall_rows * q;
+      Item it;
+      it.c_off = g.out_off[c] + (r0 >> 3) * tile_row;
+      it.cin_off = cin >= 0 ? cin + (r0 >> 3) * tile_row : -1;
+      it.p0r8 = g.out_p0[c] | (static_cast<int64_t>(r0 >> 3) << 48);
+      it.np = g.out_np[c];
+      it.rows = static_cast<int16_t>(nt > 1 ? min(g.tall_rows, m - r0) : m);
+      it.n = static_cast<int16_t>(n);
+      g.items[at + q] = it;
+    }
+  }
+  }  // split == 0
 }
 
 // K-panel work items (L2 blocking of long product chains):
@@ -902,11 +941,17 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     S.c_blocks_in = Cm.nblk;
     if (x.timing) BT_CUDA(cudaEventRecord(x.ev[0], st));
     const int64_t M = Cm.nbr, N = Cm.nbc;
-    // fill pass: 3 ints per column (counts, cursors, touched list) + bitmap
-    size_t row_smem = static_cast<size_t>(N) * 12 + 4 * ((N + 31) / 32);
-    // the fill pass's rank emission needs 8 more bytes per column
-    const bool colmask = N <= 4096 && env_int("BT_COLMASK", 1);
-    if (colmask) row_smem = 4 * ((3 * N + (N + 31) / 32 + 1) & ~int64_t(1)) + 8 * N;
+    // Symbolic passes: per-column counters of one C row live in shared memory,
+    // for a chunk of `colw` block columns at a time (rows wider than that are
+    // swept chunk by chunk; any N works).  Fill pass: 3 ints per column
+    // (counts, cursors, touched list) + bitmap, + 8 bytes per column for the
+    // rank emission (colmask) on narrow matrices, + 4 for split CTAs.
+    int64_t colw = N <= 14000 ? std::max<int64_t>(N, 1) : 8192;
+    colw = std::max<int64_t>(1, std::min<int64_t>(colw, env_int("BT_COLW", 1 << 30)));
+    const int64_t W = colw;
+    size_t row_smem = static_cast<size_t>(W) * 12 + 4 * ((W + 31) / 32);
+    const bool colmask = W <= 4096 && env_int("BT_COLMASK", 1);
+    if (colmask) row_smem = 4 * ((3 * W + (W + 31) / 32 + 1) & ~int64_t(1)) + 8 * W;
     // few long C rows (c3: 100 rows of ~2000 A entries): several fill CTAs per
     // row, each emitting a range of A chunks (+4 bytes per column of counts)
     int fill_splits = 1;
@@ -915,12 +960,11 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       fill_splits = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, chunks / 2)));
     }
     fill_splits = std::min(64, std::max(1, env_int("BT_FILL_SPLITS", fill_splits)));
-    BT_REQUIRE(row_smem <= 180 * 1024, BT_ERR_INVALID_ARGUMENT,
-               "multiply: more than 15000 block columns per C row is not supported");
-    // split CTAs need 4 more bytes per column; rows too wide for that fall
-    // back to one CTA per row instead of failing
-    if (fill_splits > 1 && row_smem + 4 * static_cast<size_t>(N) > 180 * 1024) fill_splits = 1;
-    if (fill_splits > 1) row_smem += 4 * static_cast<size_t>(N);
+    BT_REQUIRE(row_smem <= 180 * 1024, BT_ERR_INTERNAL, "multiply: column chunk too wide");
+    // split CTAs need 4 more bytes per column; if that does not fit, one CTA
+    // per row
+    if (fill_splits > 1 && row_smem + 4 * static_cast<size_t>(W) > 180 * 1024) fill_splits = 1;
+    if (fill_splits > 1) row_smem += 4 * static_cast<size_t>(W);
 
     // ---- norms for the eps filter, cached with the stores: a
     // store's norms are computed once after it changes (both in one launch
@@ -968,6 +1012,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.colmask = colmask;
     ra.tall_rows = env_int("BT_TALL_ROWS", 32) == 24 ? 24 : 32;
     ra.splits = fill_splits;
+    ra.colw = colw;
     {
       // column bands: when A and B together overflow a comfortable share of L2
       // (but are not in the K-panel regime below), sweep C in bands of B
@@ -1002,7 +1047,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.totals = tot;
     ra.class_items = tot + 3;
     if (M > 0) {
-      const size_t sm1 = static_cast<size_t>(N) * 8 + 4 * ((N + 31) / 32);
+      const size_t sm1 = static_cast<size_t>(W) * 8 + 4 * ((W + 31) / 32);
       // static + dynamic shared memory may exceed the 48 KB default: always opt in
       ensure_dyn_smem(reinterpret_cast<const void*>(k_row_count), sm1);
       k_row_count<<<static_cast<unsigned>(M), kChunkA, sm1, st>>>(ra);
