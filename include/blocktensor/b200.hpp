@@ -9,8 +9,14 @@
 //   grid.hpp:17-69        ProcessGrid
 //   comm.hpp:152-397      SimComm (+ Ledger, TrafficCounters): the device group --
 //                         every rank of the grid is a virtual rank on this
-//                         process's GPU (or, via SimComm::nccl, one rank per process)
-//   matrix.hpp:26-418     Axis, DistMatrix, new_matrix, new_matrix_round_robin
+//                         process's GPU, or (SimComm(grid, device, rank, NcclId))
+//                         one rank per process over NCCL
+//   matrix.hpp:26-418     Axis (explicit and functional), LocalStore (a view),
+//                         DistMatrix (+ local, put_block_at, get_block_at,
+//                         for_each_global), new_matrix, new_matrix_round_robin,
+//                         redistribute, redistribute_add
+//   io.hpp:22-198         FileFormat, MatrixData, read/write_matrix_{text,binary},
+//                         to_dist_matrix, read_matrix_file, write_matrix_file
 //   multiply_cannon.hpp   multiply_cannon
 //   (SPEC tensor module) SparseTensor, contract, mixed_radix
 //   multiply_rect.hpp     Algorithm, multiply_reduce_case1, multiply_virtual_case2,
@@ -31,7 +37,15 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <functional>
+#include <istream>
 #include <map>
+#include <ostream>
+#include <sstream>
+#include <charconv>
+#include <tuple>
+#include <unistd.h>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -217,8 +231,23 @@ class Ledger {
 
 class DistMatrix;
 
-// The device group: SimComm(grid) puts every rank of `grid` on one GPU of this
-// process (device BT_DEVICE, default 0) as virtual ranks.
+// NCCL unique id of a one-process-per-GPU group (128 bytes, created by rank 0
+// and handed to every rank by the caller: a file, MPI, torch.distributed ...)
+struct NcclId {
+  unsigned char bytes[128] = {};
+  static NcclId create() {
+    NcclId id;
+    detail::check(bt_get_unique_id(id.bytes));
+    return id;
+  }
+};
+
+// The device group (comm.hpp:152-397).
+//  * SimComm(grid): every rank of `grid` is a virtual rank on one GPU of this
+//    process -- the reference's one-process SimComm, messages are device copies.
+//  * SimComm(grid, device, rank, id): one rank per process over NCCL (NVLink /
+//    NVSwitch); this process owns rank `rank` of grid.size() ranks on `device`.
+// Both keep the reference's Ledger (comm.hpp:60-150) of the local ranks.
 class SimComm {
  public:
   explicit SimComm(ProcessGrid grid, Schedule = Schedule::parallel, int device = 0)
@@ -227,6 +256,26 @@ class SimComm {
     detail::check(bt_grid_create(ctx_, grid_.size(), &g_));
     current() = this;
   }
+  SimComm(ProcessGrid grid, int device, int rank, const NcclId& id) : grid_(std::move(grid)) {
+    detail::check(bt_ctx_create(device, grid_.size(), rank, id.bytes, &ctx_));
+    detail::check(bt_grid_create(ctx_, grid_.size(), &g_));
+    current() = this;
+  }
+  // this process's ranks: all of them (virtual ranks) or its own (NCCL)
+  std::vector<int> local_ranks() const {
+    int n = 0, first = 0, nl = 0;
+    detail::check(bt_grid_info(g_, &n, &first, &nl));
+    std::vector<int> r;
+    for (int t = 0; t < nl; ++t) r.push_back(first + t);
+    return r;
+  }
+  bool is_local(int rank) const {
+    int n = 0, first = 0, nl = 0;
+    detail::check(bt_grid_info(g_, &n, &first, &nl));
+    return rank >= first && rank < first + nl;
+  }
+  // waits for all device work of this process (incl. asynchronous exports)
+  void sync() const { detail::check(bt_ctx_sync(ctx_)); }
   SimComm(const SimComm&) = delete;
   SimComm& operator=(const SimComm&) = delete;
   ~SimComm() {
@@ -252,11 +301,14 @@ class SimComm {
 };
 
 // ------------------------------------------------------------------ matrix
+// Axis (matrix.hpp:26-130): block sizes and grid coordinates of one matrix
+// dimension, explicit arrays or functions (Axis::functional keeps no O(N)
+// arrays on the host; the device store holds the sizes it needs).
 class Axis {
  public:
   Axis() = default;
   Axis(const Blocking& b, std::vector<int> dist, int extent)
-      : blocking_(b), dist_(std::move(dist)), extent_(extent) {
+      : n_blocks_(b.n_blocks()), extent_(extent), blocking_(b), dist_(std::move(dist)) {
     if (static_cast<std::int64_t>(dist_.size()) != b.n_blocks())
       throw invalid_argument("Axis: distribution length does not match block count");
     for (int c : dist_)
@@ -267,20 +319,123 @@ class Axis {
     for (std::size_t i = 0; i < d.size(); ++i) d[i] = static_cast<int>(i % extent);
     return Axis(b, std::move(d), extent);
   }
-  std::int64_t n_blocks() const noexcept { return blocking_.n_blocks(); }
+  static Axis functional(std::int64_t n_blocks, std::function<int(std::int64_t)> size_fn,
+                         std::function<int(std::int64_t)> dist_fn, int extent) {
+    if (n_blocks < 0 || extent < 1) throw invalid_argument("Axis: bad functional axis");
+    Axis a;
+    a.n_blocks_ = n_blocks;
+    a.extent_ = extent;
+    a.size_fn_ = std::move(size_fn);
+    a.dist_fn_ = std::move(dist_fn);
+    return a;
+  }
+  bool is_explicit() const noexcept { return !size_fn_; }
+  std::int64_t n_blocks() const noexcept { return n_blocks_; }
   int extent() const noexcept { return extent_; }
-  int size(std::int64_t b) const { return blocking_.size(b); }
-  int dist(std::int64_t b) const { return dist_.at(static_cast<std::size_t>(b)); }
-  std::int64_t total_elements() const { return blocking_.total(); }
-  const Blocking& blocking() const noexcept { return blocking_; }
-  const std::vector<int>& dists() const noexcept { return dist_; }
-  bool same_blocking(const Axis& o) const { return blocking_ == o.blocking_; }
-  bool same_distribution(const Axis& o) const { return extent_ == o.extent_ && dist_ == o.dist_; }
+  int size(std::int64_t b) const {
+    check_block(b);
+    return is_explicit() ? blocking_.size(b) : size_fn_(b);
+  }
+  int dist(std::int64_t b) const {
+    check_block(b);
+    const int c = is_explicit() ? dist_[static_cast<std::size_t>(b)] : dist_fn_(b);
+    if (c < 0 || c >= extent_) throw invalid_argument("Axis: distribution coordinate out of grid range");
+    return c;
+  }
+  std::int64_t total_elements() const {
+    if (is_explicit()) return blocking_.total();
+    std::int64_t t = 0;
+    for (std::int64_t b = 0; b < n_blocks_; ++b) t += size_fn_(b);
+    return t;
+  }
+  // host index entries this axis keeps resident (0 for a functional axis)
+  std::int64_t index_entries() const noexcept {
+    return is_explicit() ? 2 * n_blocks_ : 0;
+  }
+  // the blocking (materialized on demand for a functional axis)
+  Blocking blocking() const {
+    if (is_explicit()) return blocking_;
+    std::vector<int> v(static_cast<std::size_t>(n_blocks_));
+    for (std::int64_t b = 0; b < n_blocks_; ++b) v[static_cast<std::size_t>(b)] = size_fn_(b);
+    return Blocking(std::move(v));
+  }
+  std::vector<int> dists() const {
+    if (is_explicit()) return dist_;
+    std::vector<int> v(static_cast<std::size_t>(n_blocks_));
+    for (std::int64_t b = 0; b < n_blocks_; ++b) v[static_cast<std::size_t>(b)] = dist(b);
+    return v;
+  }
+  bool same_blocking(const Axis& o) const {
+    if (n_blocks_ != o.n_blocks_) return false;
+    for (std::int64_t b = 0; b < n_blocks_; ++b)
+      if (size(b) != o.size(b)) return false;
+    return true;
+  }
+  bool same_distribution(const Axis& o) const {
+    if (n_blocks_ != o.n_blocks_ || extent_ != o.extent_) return false;
+    for (std::int64_t b = 0; b < n_blocks_; ++b)
+      if (dist(b) != o.dist(b)) return false;
+    return true;
+  }
 
  private:
+  void check_block(std::int64_t b) const {
+    if (b < 0 || b >= n_blocks_) throw invalid_argument("Axis: block index out of range");
+  }
+  std::int64_t n_blocks_ = 0;
+  int extent_ = 1;
   Blocking blocking_;
   std::vector<int> dist_;
-  int extent_ = 1;
+  std::function<int(std::int64_t)> size_fn_, dist_fn_;
+};
+
+// One rank's store (LocalStore, matrix.hpp:137-275), a view onto the device
+// store: the visitors copy the blocks to the host once per call, in (row, col)
+// order, as DenseBlocks.
+class LocalStore {
+ public:
+  LocalStore(bt_mat* s, const Axis* rows, const Axis* cols) : s_(s), rows_(rows), cols_(cols) {}
+  std::int64_t stored_blocks() const { return info().first; }
+  std::int64_t stored_elements() const { return info().second; }
+  template <class Fn>
+  void for_each(Fn&& fn) const {
+    std::vector<std::int64_t> bi, bj;
+    std::vector<double> v;
+    pull(bi, bj, v);
+    std::size_t off = 0;
+    for (std::size_t t = 0; t < bi.size(); ++t) {
+      const int m = rows_->size(bi[t]), n = cols_->size(bj[t]);
+      DenseBlock b(m, n, std::vector<double>(v.begin() + off, v.begin() + off + std::size_t(m) * n));
+      off += std::size_t(m) * n;
+      fn(bi[t], bj[t], static_cast<const DenseBlock&>(b));
+    }
+  }
+  template <class Fn>
+  void for_each_in_row_range(std::int64_t i, std::int64_t col_begin, std::int64_t col_end,
+                             Fn&& fn) const {
+    for_each([&](std::int64_t r, std::int64_t c, const DenseBlock& b) {
+      if (r == i && c >= col_begin && c < col_end) fn(r, c, b);
+    });
+  }
+  bt_mat* handle() const noexcept { return s_; }
+
+ private:
+  std::pair<std::int64_t, std::int64_t> info() const {
+    int64_t b = 0, e = 0;
+    detail::check(bt_mat_info(s_, &b, &e));
+    return {b, e};
+  }
+  void pull(std::vector<std::int64_t>& bi, std::vector<std::int64_t>& bj,
+            std::vector<double>& v) const {
+    const auto ie = info();
+    bi.resize(static_cast<std::size_t>(ie.first));
+    bj.resize(static_cast<std::size_t>(ie.first));
+    v.resize(static_cast<std::size_t>(ie.second));
+    if (ie.first) detail::check(bt_mat_export(s_, bi.data(), bj.data(), v.data()));
+  }
+  bt_mat* s_;
+  const Axis* rows_;
+  const Axis* cols_;
 };
 
 class DistMatrix {
@@ -291,10 +446,12 @@ class DistMatrix {
     if (grid_.ndims() != 2) throw invalid_argument("DistMatrix: grid must be 2-dimensional");
     if (rows_.extent() != grid_.dim(0) || cols_.extent() != grid_.dim(1))
       throw invalid_argument("DistMatrix: axis extents do not match the grid");
-    std::vector<int32_t> rs(rows_.blocking().sizes().begin(), rows_.blocking().sizes().end());
-    std::vector<int32_t> cs(cols_.blocking().sizes().begin(), cols_.blocking().sizes().end());
-    std::vector<int32_t> rd(rows_.dists().begin(), rows_.dists().end());
-    std::vector<int32_t> cd(cols_.dists().begin(), cols_.dists().end());
+    const Blocking rb = rows_.blocking(), cb = cols_.blocking();
+    const std::vector<int> rdv = rows_.dists(), cdv = cols_.dists();
+    std::vector<int32_t> rs(rb.sizes().begin(), rb.sizes().end());
+    std::vector<int32_t> cs(cb.sizes().begin(), cb.sizes().end());
+    std::vector<int32_t> rd(rdv.begin(), rdv.end());
+    std::vector<int32_t> cd(cdv.begin(), cdv.end());
     bt_dmat* h = nullptr;
     detail::check(bt_dmat_create(comm_->handle(), static_cast<int64_t>(rs.size()), rs.data(),
                                  static_cast<int64_t>(cs.size()), cs.data(), grid_.dim(0),
@@ -312,10 +469,50 @@ class DistMatrix {
   int nranks() const noexcept { return grid_.size(); }
   bt_dmat* handle() const noexcept { return h_.get(); }
 
+  SimComm* comm() const noexcept { return comm_; }
+
+  // the store of rank `rank` (matrix.hpp:294-295); ownership_error when the
+  // rank lives in another process
+  LocalStore local(int rank) const {
+    bt_mat* s = nullptr;
+    detail::check(bt_dmat_local(h_.get(), rank, &s));
+    return LocalStore(s, &rows_, &cols_);
+  }
+
   void put_block(std::int64_t i, std::int64_t j, DenseBlock block, bool accumulate = false) {
     if (block.rows != rows_.size(i) || block.cols != cols_.size(j))
       throw invalid_argument("put_block: block dimensions do not match the slot");
     detail::check(bt_dmat_put_blocks(h_.get(), 1, &i, &j, block.values.data(), accumulate ? 1 : 0));
+  }
+
+  // ownership-checked variant used by rank workers (matrix.hpp:312-321)
+  void put_block_at(int rank, std::int64_t i, std::int64_t j, DenseBlock block,
+                    bool accumulate = false) {
+    const int owner = owner_rank(i, j);
+    if (owner != rank)
+      throw ownership_error("put_block: rank " + std::to_string(rank) + " does not own block (" +
+                            std::to_string(i) + "," + std::to_string(j) + "), rank " +
+                            std::to_string(owner) + " does");
+    put_block(i, j, std::move(block), accumulate);
+  }
+
+  const DenseBlock* get_block_at(int rank, std::int64_t i, std::int64_t j) const {
+    const int owner = owner_rank(i, j);
+    if (owner != rank)
+      throw ownership_error("get_block: rank " + std::to_string(rank) + " does not own block (" +
+                            std::to_string(i) + "," + std::to_string(j) + "), rank " +
+                            std::to_string(owner) + " does");
+    return get_block(i, j);
+  }
+
+  // every stored block of this process's ranks in (rank, row, col) order
+  // (matrix.hpp:363-368)
+  template <class Fn>
+  void for_each_global(Fn&& fn) const {
+    for (int r = 0; r < grid_.size(); ++r) {
+      if (!comm_->is_local(r)) continue;
+      local(r).for_each([&](std::int64_t i, std::int64_t j, const DenseBlock& b) { fn(r, i, j, b); });
+    }
   }
 
   const DenseBlock* get_block(std::int64_t i, std::int64_t j) const {
@@ -406,130 +603,221 @@ inline void filter(DistMatrix& m, double eps) {
   }
 }
 
+// ----------------------------------------------------------- redistribution
+// redistribute (matrix.hpp:567-600): `src` onto a new layout on the device
+// (owner split + NVLink/device exchange + merge), each block moved at most
+// once and only blocks that change ranks charged to the ledger; with
+// `transpose`, block (i,j) lands transposed at (j,i).
+inline DistMatrix redistribute(SimComm& comm, const DistMatrix& src, Axis new_rows, Axis new_cols,
+                               const ProcessGrid& new_grid, bool transpose = false,
+                               const std::string& phase = "redistribute") {
+  if (!transpose) {
+    if (!src.rows().same_blocking(new_rows) || !src.cols().same_blocking(new_cols))
+      throw invalid_argument("redistribute: target blockings do not match the source");
+  } else if (!src.rows().same_blocking(new_cols) || !src.cols().same_blocking(new_rows)) {
+    throw invalid_argument("redistribute: transposed target blockings do not match");
+  }
+  if (comm.nranks() < src.grid().size() || comm.nranks() < new_grid.size())
+    throw invalid_argument("redistribute: communicator smaller than the involved grids");
+  DistMatrix dst(std::move(new_rows), std::move(new_cols), new_grid, &comm);
+  detail::check(bt_redistribute(src.handle(), dst.handle(), transpose ? 1 : 0, 0, phase.c_str()));
+  return dst;
+}
+
+// redistribute_add (matrix.hpp:604-622): every stored block of `src` routed
+// into `dst`, accumulating into blocks already present.
+inline void redistribute_add(SimComm& comm, const DistMatrix& src, DistMatrix& dst,
+                             const std::string& phase = "redistribute") {
+  if (!src.rows().same_blocking(dst.rows()) || !src.cols().same_blocking(dst.cols()))
+    throw invalid_argument("redistribute_add: blockings do not conform");
+  if (comm.nranks() < src.grid().size() || comm.nranks() < dst.grid().size())
+    throw invalid_argument("redistribute_add: communicator smaller than the involved grids");
+  detail::check(bt_redistribute(src.handle(), dst.handle(), 0, 1, phase.c_str()));
+}
+
 // -------------------------------------------------------------- fixture I/O
-// Binary matrix files in the reference's format (io.hpp:132-178): little-endian
-// int64 header rows, cols, nblkrows, nblkcols, the two blocking lists, then per
-// block i, j and the row-major values, blocks in (i, j) order.
+// Fixture files in the reference's formats (io.hpp:22-198), same signatures:
+//  text   "rows cols nblkrows nblkcols" / row block sizes / column block sizes /
+//         per block "i j" and its row-major values (shortest round-trip
+//         decimal, std::to_chars);
+//  binary the same fields as little-endian int64 / 8-byte doubles.
+// Blocks are written in (i, j) order.  A DistMatrix's blocks are read from the
+// device; with one rank per process (NCCL) a writer sees only its own ranks'
+// blocks.
+enum class FileFormat { text, binary };
+
 struct MatrixData {
-  Blocking rows, cols;
-  std::vector<std::int64_t> bi, bj;
-  std::vector<double> values;  // blocks concatenated in listed order
+  Blocking rows;
+  Blocking cols;
+  std::vector<std::tuple<std::int64_t, std::int64_t, DenseBlock>> blocks;
 };
 
 namespace detail {
-inline std::int64_t rd64(std::FILE* f, bool& ok) {
+inline std::string format_double(double v) {
+  char buf[64];
+  auto res = std::to_chars(buf, buf + sizeof(buf), v);
+  if (res.ec != std::errc()) throw error("format_double failed");
+  return std::string(buf, res.ptr);
+}
+inline void put_i64(std::ostream& os, std::int64_t v) {
   unsigned char b[8];
-  ok = ok && std::fread(b, 1, 8, f) == 8;
+  const auto u = static_cast<std::uint64_t>(v);
+  for (int t = 0; t < 8; ++t) b[t] = static_cast<unsigned char>((u >> (8 * t)) & 0xff);
+  os.write(reinterpret_cast<const char*>(b), 8);
+}
+inline bool get_i64(std::istream& is, std::int64_t& v) {
+  unsigned char b[8];
+  if (!is.read(reinterpret_cast<char*>(b), 8)) return false;
   std::uint64_t u = 0;
   for (int t = 7; t >= 0; --t) u = (u << 8) | b[t];
-  return static_cast<std::int64_t>(u);
+  v = static_cast<std::int64_t>(u);
+  return true;
 }
-inline void wr64(std::FILE* f, std::uint64_t u) {
-  unsigned char b[8];
-  for (int t = 0; t < 8; ++t) b[t] = static_cast<unsigned char>((u >> (8 * t)) & 0xff);
-  std::fwrite(b, 1, 8, f);
+inline void put_f64(std::ostream& os, double v) {
+  std::uint64_t u;
+  std::memcpy(&u, &v, 8);
+  put_i64(os, static_cast<std::int64_t>(u));
+}
+inline bool get_f64(std::istream& is, double& v) {
+  std::int64_t i;
+  if (!get_i64(is, i)) return false;
+  const auto u = static_cast<std::uint64_t>(i);
+  std::memcpy(&v, &u, 8);
+  return true;
+}
+// this process's blocks in (i, j) order
+inline std::vector<std::tuple<std::int64_t, std::int64_t, DenseBlock>> sorted_blocks(
+    const DistMatrix& m) {
+  std::vector<std::tuple<std::int64_t, std::int64_t, DenseBlock>> all;
+  m.for_each_global([&](int, std::int64_t i, std::int64_t j, const DenseBlock& b) {
+    all.emplace_back(i, j, b);
+  });
+  std::sort(all.begin(), all.end(), [](const auto& x, const auto& y) {
+    return std::make_pair(std::get<0>(x), std::get<1>(x)) <
+           std::make_pair(std::get<0>(y), std::get<1>(y));
+  });
+  return all;
+}
+inline MatrixData read_header(std::istream& is, bool binary) {
+  std::int64_t rows = 0, cols = 0, nbr = 0, nbc = 0;
+  if (binary) {
+    if (!get_i64(is, rows) || !get_i64(is, cols) || !get_i64(is, nbr) || !get_i64(is, nbc))
+      throw error("matrix file: bad binary header");
+  } else if (!(is >> rows >> cols >> nbr >> nbc)) {
+    throw error("matrix file: bad header");
+  }
+  if (nbr < 0 || nbc < 0) throw error("matrix file: bad header");
+  std::vector<int> rs(static_cast<std::size_t>(nbr)), cs(static_cast<std::size_t>(nbc));
+  for (int pass = 0; pass < 2; ++pass)
+    for (auto& x : pass ? cs : rs) {
+      std::int64_t v = 0;
+      const bool ok = binary ? get_i64(is, v) : static_cast<bool>(is >> v);
+      if (!ok) throw error(pass ? "matrix file: bad column blocking" : "matrix file: bad row blocking");
+      x = static_cast<int>(v);
+    }
+  MatrixData d{Blocking(rs), Blocking(cs), {}};
+  if (d.rows.total() != rows || d.cols.total() != cols)
+    throw error("matrix file: blocking does not sum to the header dimensions");
+  return d;
 }
 }  // namespace detail
 
-inline MatrixData read_matrix_binary(const std::string& path) {
-  std::FILE* f = std::fopen(path.c_str(), "rb");
-  if (!f) throw error("cannot open " + path);
-  bool ok = true;
-  const std::int64_t rows = detail::rd64(f, ok), cols = detail::rd64(f, ok);
-  const std::int64_t nbr = detail::rd64(f, ok), nbc = detail::rd64(f, ok);
-  if (!ok || nbr < 0 || nbc < 0) {
-    std::fclose(f);
-    throw error("matrix file: bad binary header");
+inline void write_matrix_text(std::ostream& os, const DistMatrix& m) {
+  os << m.rows().total_elements() << ' ' << m.cols().total_elements() << ' '
+     << m.n_block_rows() << ' ' << m.n_block_cols() << '\n';
+  for (std::int64_t b = 0; b < m.n_block_rows(); ++b)
+    os << m.rows().size(b) << (b + 1 < m.n_block_rows() ? ' ' : '\n');
+  if (m.n_block_rows() == 0) os << '\n';
+  for (std::int64_t b = 0; b < m.n_block_cols(); ++b)
+    os << m.cols().size(b) << (b + 1 < m.n_block_cols() ? ' ' : '\n');
+  if (m.n_block_cols() == 0) os << '\n';
+  for (const auto& ijb : detail::sorted_blocks(m)) {
+    os << std::get<0>(ijb) << ' ' << std::get<1>(ijb) << '\n';
+    const auto& v = std::get<2>(ijb).values;
+    for (std::size_t t = 0; t < v.size(); ++t)
+      os << detail::format_double(v[t]) << (t + 1 < v.size() ? ' ' : '\n');
   }
-  std::vector<int> rs(static_cast<std::size_t>(nbr)), cs(static_cast<std::size_t>(nbc));
-  for (auto& x : rs) x = static_cast<int>(detail::rd64(f, ok));
-  for (auto& x : cs) x = static_cast<int>(detail::rd64(f, ok));
-  if (!ok) {
-    std::fclose(f);
-    throw error("matrix file: bad blocking");
-  }
-  MatrixData d{Blocking(rs), Blocking(cs), {}, {}, {}};
-  if (d.rows.total() != rows || d.cols.total() != cols) {
-    std::fclose(f);
-    throw error("matrix file: blocking does not sum to the header dimensions");
-  }
-  for (;;) {
-    bool more = true;
-    const std::int64_t i = detail::rd64(f, more);
-    if (!more) break;
-    const std::int64_t j = detail::rd64(f, ok);
-    if (!ok || i < 0 || i >= nbr || j < 0 || j >= nbc) {
-      std::fclose(f);
+}
+
+inline MatrixData read_matrix_data_text(std::istream& is) {
+  MatrixData d = detail::read_header(is, false);
+  std::int64_t i, j;
+  while (is >> i >> j) {
+    if (i < 0 || i >= d.rows.n_blocks() || j < 0 || j >= d.cols.n_blocks())
       throw error("matrix file: block index out of range");
-    }
-    d.bi.push_back(i);
-    d.bj.push_back(j);
-    const std::int64_t n = std::int64_t(rs[i]) * cs[j];
-    for (std::int64_t t = 0; t < n; ++t) {
-      const std::int64_t u = detail::rd64(f, ok);
-      double v;
-      std::memcpy(&v, &u, 8);
-      d.values.push_back(v);
-    }
-    if (!ok) {
-      std::fclose(f);
-      throw error("matrix file: truncated block values");
-    }
+    DenseBlock b(d.rows.size(i), d.cols.size(j));
+    for (auto& v : b.values)
+      if (!(is >> v)) throw error("matrix file: truncated block values");
+    d.blocks.emplace_back(i, j, std::move(b));
   }
-  std::fclose(f);
   return d;
 }
 
-// to_dist_matrix (io.hpp:181-185): round-robin on `grid`, one batched upload
-inline DistMatrix to_dist_matrix(const MatrixData& d, const ProcessGrid& grid) {
-  DistMatrix m = new_matrix_round_robin(d.rows, d.cols, grid);
-  if (!d.bi.empty())
-    detail::check(bt_dmat_put_blocks(m.handle(), static_cast<int64_t>(d.bi.size()), d.bi.data(),
-                                     d.bj.data(), d.values.data(), 0));
+inline void write_matrix_binary(std::ostream& os, const DistMatrix& m) {
+  detail::put_i64(os, m.rows().total_elements());
+  detail::put_i64(os, m.cols().total_elements());
+  detail::put_i64(os, m.n_block_rows());
+  detail::put_i64(os, m.n_block_cols());
+  for (std::int64_t b = 0; b < m.n_block_rows(); ++b) detail::put_i64(os, m.rows().size(b));
+  for (std::int64_t b = 0; b < m.n_block_cols(); ++b) detail::put_i64(os, m.cols().size(b));
+  for (const auto& ijb : detail::sorted_blocks(m)) {
+    detail::put_i64(os, std::get<0>(ijb));
+    detail::put_i64(os, std::get<1>(ijb));
+    for (double v : std::get<2>(ijb).values) detail::put_f64(os, v);
+  }
+}
+
+inline MatrixData read_matrix_data_binary(std::istream& is) {
+  MatrixData d = detail::read_header(is, true);
+  std::int64_t i;
+  while (detail::get_i64(is, i)) {
+    std::int64_t j;
+    if (!detail::get_i64(is, j)) throw error("matrix file: truncated block header");
+    if (i < 0 || i >= d.rows.n_blocks() || j < 0 || j >= d.cols.n_blocks())
+      throw error("matrix file: block index out of range");
+    DenseBlock b(d.rows.size(i), d.cols.size(j));
+    for (auto& v : b.values)
+      if (!detail::get_f64(is, v)) throw error("matrix file: truncated block values");
+    d.blocks.emplace_back(i, j, std::move(b));
+  }
+  return d;
+}
+
+// to_dist_matrix (io.hpp:181-185): round robin on `grid`; the blocks this
+// process owns go to the device in one batched upload (with one rank per
+// process every process reads the file and keeps its share)
+inline DistMatrix to_dist_matrix(MatrixData&& data, const ProcessGrid& grid) {
+  DistMatrix m = new_matrix_round_robin(data.rows, data.cols, grid);
+  std::vector<std::int64_t> bi, bj;
+  std::vector<double> v;
+  for (auto& t : data.blocks) {
+    const std::int64_t i = std::get<0>(t), j = std::get<1>(t);
+    if (!m.comm()->is_local(m.owner_rank(i, j))) continue;
+    const DenseBlock& b = std::get<2>(t);
+    if (b.rows != data.rows.size(i) || b.cols != data.cols.size(j))
+      throw invalid_argument("put_block: block dimensions do not match the slot");
+    bi.push_back(i);
+    bj.push_back(j);
+    v.insert(v.end(), b.values.begin(), b.values.end());
+  }
+  if (!bi.empty())
+    detail::check(bt_dmat_put_blocks(m.handle(), static_cast<int64_t>(bi.size()), bi.data(),
+                                     bj.data(), v.data(), 0));
+  data.blocks.clear();
   return m;
 }
 
-// write_matrix_binary (io.hpp:134-148) for the blocks held by this process
-inline void write_matrix_binary(const std::string& path, const DistMatrix& m) {
-  std::vector<std::int64_t> bi, bj;
-  std::vector<double> vals;
-  std::vector<std::pair<std::pair<std::int64_t, std::int64_t>, std::size_t>> order;
-  std::vector<std::vector<double>> blocks;
-  for (int r = 0; r < m.nranks(); ++r) {
-    bt_mat* s = nullptr;
-    if (bt_dmat_local(m.handle(), r, &s) != BT_OK) continue;
-    int64_t nb = 0, ne = 0;
-    detail::check(bt_mat_info(s, &nb, &ne));
-    std::vector<std::int64_t> i(nb), j(nb);
-    std::vector<double> v(ne);
-    detail::check(bt_mat_export(s, i.data(), j.data(), v.data()));
-    std::size_t off = 0;
-    for (int64_t t = 0; t < nb; ++t) {
-      const std::size_t n = std::size_t(m.rows().size(i[t])) * m.cols().size(j[t]);
-      order.push_back({{i[t], j[t]}, blocks.size()});
-      blocks.emplace_back(v.begin() + off, v.begin() + off + n);
-      off += n;
-    }
-  }
-  std::sort(order.begin(), order.end());
-  std::FILE* f = std::fopen(path.c_str(), "wb");
-  if (!f) throw error("cannot open " + path + " for writing");
-  detail::wr64(f, m.rows().total_elements());
-  detail::wr64(f, m.cols().total_elements());
-  detail::wr64(f, m.n_block_rows());
-  detail::wr64(f, m.n_block_cols());
-  for (std::int64_t b = 0; b < m.n_block_rows(); ++b) detail::wr64(f, m.rows().size(b));
-  for (std::int64_t b = 0; b < m.n_block_cols(); ++b) detail::wr64(f, m.cols().size(b));
-  for (const auto& o : order) {
-    detail::wr64(f, o.first.first);
-    detail::wr64(f, o.first.second);
-    for (double v : blocks[o.second]) {
-      std::uint64_t u;
-      std::memcpy(&u, &v, 8);
-      detail::wr64(f, u);
-    }
-  }
-  std::fclose(f);
+inline void write_matrix_file(const std::string& path, const DistMatrix& m, FileFormat format) {
+  std::ofstream os(path, format == FileFormat::binary ? std::ios::binary : std::ios::out);
+  if (!os) throw error("cannot open " + path + " for writing");
+  if (format == FileFormat::binary) write_matrix_binary(os, m); else write_matrix_text(os, m);
+  if (!os) throw error("write to " + path + " failed");
+}
+
+inline MatrixData read_matrix_file(const std::string& path, FileFormat format) {
+  std::ifstream is(path, format == FileFormat::binary ? std::ios::binary : std::ios::in);
+  if (!is) throw error("cannot open " + path);
+  return format == FileFormat::binary ? read_matrix_data_binary(is) : read_matrix_data_text(is);
 }
 
 // -------------------------------------------------------------- cost model

@@ -246,6 +246,10 @@ class Reference:
         L.ref_res_free.argtypes = [C.c_void_p]
         L.ref_cost.argtypes = [C.c_int] + [C.c_double] * 7
         L.ref_cost.restype = C.c_double
+        L.ref_io_write.argtypes = [C.c_char_p, C.c_int, C.c_int64, _i32p, C.c_int64, _i32p,
+                                   C.c_int64, _i64p, _i64p, _f64p]
+        L.ref_io_read.argtypes = [C.c_char_p, C.c_int]
+        L.ref_io_read.restype = C.c_void_p
 
     def _err(self):
         return self.lib.ref_last_error().decode()
@@ -322,3 +326,39 @@ class Reference:
 
     def cost(self, which, m, n, k, oa, ob, oc, p) -> float:
         return self.lib.ref_cost(which, m, n, k, oa, ob, oc, p)
+
+    # -- fixture I/O with the reference's own io.hpp (fmt "text" | "binary")
+    def write_matrix_file(self, path: str, b: Blocks, fmt: str = "binary"):
+        rsz = np.ascontiguousarray(b.rsz, np.int32)
+        csz = np.ascontiguousarray(b.csz, np.int32)
+        bi = np.ascontiguousarray(b.bi, np.int64)
+        bj = np.ascontiguousarray(b.bj, np.int64)
+        v = np.ascontiguousarray(b.vals, np.float64)
+        if self.lib.ref_io_write(path.encode(), int(fmt == "binary"), len(rsz), _p(rsz, _i32p),
+                                 len(csz), _p(csz, _i32p), len(bi), _p(bi, _i64p),
+                                 _p(bj, _i64p), _p(v, _f64p)):
+            raise RuntimeError(self._err())
+
+    def read_matrix_file(self, path: str, fmt: str = "binary") -> Blocks:
+        h = self.lib.ref_io_read(path.encode(), int(fmt == "binary"))
+        if not h:
+            raise RuntimeError(self._err())
+        try:
+            # blockings from the file header (the reader validated them)
+            rsz, csz = _file_blockings(path, fmt)
+            return self._take(h, rsz, csz)
+        finally:
+            self.lib.ref_res_free(h)
+
+
+def _file_blockings(path, fmt):
+    if fmt == "binary":
+        raw = open(path, "rb").read(32)
+        nbr, nbc = np.frombuffer(raw, "<i8")[2:4]
+        data = np.fromfile(path, "<i8", count=4 + int(nbr) + int(nbc))
+        return data[4:4 + nbr].astype(np.int32), data[4 + nbr:].astype(np.int32)
+    with open(path) as f:
+        nbr, nbc = [int(x) for x in f.readline().split()][2:4]
+        rs = np.array(f.readline().split(), np.int32) if nbr else np.zeros(0, np.int32)
+        cs = np.array(f.readline().split(), np.int32) if nbc else np.zeros(0, np.int32)
+    return rs, cs

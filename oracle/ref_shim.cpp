@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "blocktensor/cost_model.hpp"
+#include "blocktensor/io.hpp"
 #include "blocktensor/matrix.hpp"
 #include "blocktensor/multiply_cannon.hpp"
 #include "blocktensor/multiply_rect.hpp"
@@ -185,6 +186,35 @@ double ref_cost(int which, double m, double n, double k, double oa, double ob, d
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1.0;
+  }
+}
+
+// Fixture I/O through the reference's own io.hpp (write_matrix_file /
+// read_matrix_file): pins the facade's readers and writers byte for byte.
+// fmt: 0 text, 1 binary.
+int ref_io_write(const char* path, int fmt, std::int64_t nbr, const std::int32_t* rsz,
+                 std::int64_t nbc, const std::int32_t* csz, std::int64_t nblk,
+                 const std::int64_t* bi, const std::int64_t* bj, const double* vals) {
+  try {
+    ProcessGrid grid({1, 1});
+    DistMatrix m = new_matrix_round_robin(make_blocking(nbr, rsz), make_blocking(nbc, csz), grid);
+    fill(m, nblk, bi, bj, vals);
+    write_matrix_file(path, m, fmt ? FileFormat::binary : FileFormat::text);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+void* ref_io_read(const char* path, int fmt) {
+  try {
+    MatrixData d = read_matrix_file(path, fmt ? FileFormat::binary : FileFormat::text);
+    DistMatrix m = to_dist_matrix(std::move(d), ProcessGrid({1, 1}));
+    return collect(m);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
   }
 }
 

@@ -59,75 +59,152 @@ __device__ __forceinline__ void compose(const TensorShape& s, const TensorMap& m
   for (int q = m.nr; q < m.ndim; ++q) col = col * s.nb[m.dims[q]] + coord[m.dims[q]];
 }
 
-// destination key (row * ncols + col) of every source entry
+// destination key (row * ncols + col) of every source entry: one thread per
+// stored block (its row by a binary search of the row pointer)
 __global__ void k_remap_keys(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                             int64_t nbr, TensorShape s, TensorMap from, TensorMap to,
-                             int64_t dst_nbc, uint64_t* __restrict__ keys,
+                             int64_t nbr, int64_t nblk, TensorShape s, TensorMap from,
+                             TensorMap to, int64_t dst_nbc, uint64_t* __restrict__ keys,
                              int32_t* __restrict__ idx) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nbr) return;
-  for (int32_t e = rp[i]; e < rp[i + 1]; ++e) {
-    int64_t c[kMaxRank];
-    decompose(s, from, i, col[e], c);
-    int64_t r2, c2;
-    compose(s, to, c, r2, c2);
-    keys[e] = static_cast<uint64_t>(r2 * dst_nbc + c2);
-    idx[e] = static_cast<int32_t>(e);
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nblk) return;
+  int64_t lo = 0, hi = nbr;  // last row with rp[row] <= e
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (rp[mid] <= e) lo = mid; else hi = mid;
   }
+  int64_t c[kMaxRank];
+  decompose(s, from, lo, col[e], c);
+  int64_t r2, c2;
+  compose(s, to, c, r2, c2);
+  keys[e] = static_cast<uint64_t>(r2 * dst_nbc + c2);
+  idx[e] = static_cast<int32_t>(e);
 }
 
+// column of every sorted entry, per-row counts, T8 slot length and element count
 __global__ void k_remap_rows(const uint64_t* __restrict__ keys, int64_t n, int64_t dst_nbc,
-                             int32_t* __restrict__ row_cnt, int32_t* __restrict__ out_col) {
+                             const int32_t* __restrict__ rsz, const int32_t* __restrict__ csz,
+                             int32_t* __restrict__ row_cnt, int32_t* __restrict__ out_col,
+                             int64_t* __restrict__ len, int64_t* __restrict__ elems) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  atomicAdd(&row_cnt[keys[t] / dst_nbc], 1);
-  out_col[t] = static_cast<int32_t>(keys[t] % dst_nbc);
+  if (t > n) return;
+  if (t == n) {  // scan sentinels: the totals land in element n
+    len[n] = 0;
+    elems[n] = 0;
+    return;
+  }
+  const int64_t r = static_cast<int64_t>(keys[t] / dst_nbc), c = static_cast<int64_t>(keys[t] % dst_nbc);
+  atomicAdd(&row_cnt[r], 1);
+  out_col[t] = static_cast<int32_t>(c);
+  len[t] = t8_size(rsz[r], csz[c]);
+  elems[t] = static_cast<int64_t>(rsz[r]) * csz[c];
 }
 
-// element permutation of one block: destination (r2, c2) <- source (r, c)
-__global__ void k_remap_vals(const uint64_t* __restrict__ keys, const int32_t* __restrict__ src_e,
-                             const int64_t* __restrict__ src_off, const int64_t* __restrict__ dst_off,
-                             int64_t n, int64_t dst_nbc, TensorShape s, TensorMap from,
-                             TensorMap to, const double* __restrict__ src, double* __restrict__ dst) {
+// Element permutation of one block, written in destination T8 storage order
+// (coalesced stores, padding written as zeros) and gathered from the source
+// block (L1/L2 resident).  The source position is separable:
+//   r1 = RA[r2] + RB[c2],  c1 = CA[r2] + CB[c2]
+// because a mixed-radix index is a sum of per-dimension terms and every
+// dimension's element offset comes either from the destination row r2 or from
+// the destination column c2.  The four tables are built per block in shared
+// memory (R2 + C2 entries each), so the inner loop is two lookups and adds.
+// tab_n: entries per table (dynamic shared memory 16 * tab_n bytes), at least
+// the largest R2 and C2 of the launch; 0 = no tables (per-element decomposition)
+constexpr int kRemapTabMax = 3072;
+__global__ void __launch_bounds__(128) k_remap_vals(
+    const uint64_t* __restrict__ keys, const int32_t* __restrict__ src_e,
+    const int64_t* __restrict__ src_off, const int64_t* __restrict__ dst_off, int64_t n,
+    int64_t dst_nbc, TensorShape s, TensorMap from, TensorMap to, const double* __restrict__ src,
+    double* __restrict__ dst, int tab_n) {
+  extern __shared__ int32_t tab[];
   const int64_t t = blockIdx.x;
   if (t >= n) return;
   int64_t c[kMaxRank];
   decompose(s, to, static_cast<int64_t>(keys[t] / dst_nbc), static_cast<int64_t>(keys[t] % dst_nbc), c);
   int ext[kMaxRank];
-  int total = 1;
-  for (int d = 0; d < s.ndim; ++d) {
-    ext[d] = s.sz[d][c[d]];
-    total *= ext[d];
+  for (int d = 0; d < s.ndim; ++d) ext[d] = s.sz[d][c[d]];
+  // block shapes under both maps; strides of every dim in the source map
+  int C1 = 1, R2 = 1, C2 = 1;
+  int sr[kMaxRank] = {0, 0, 0, 0}, sc[kMaxRank] = {0, 0, 0, 0};
+  for (int q = from.ndim - 1, acc = 1; q >= from.nr; --q) {
+    sc[from.dims[q]] = acc;
+    acc *= ext[from.dims[q]];
+    C1 = acc;
   }
-  // block shapes under both maps
-  int R1 = 1, C1 = 1, R2 = 1, C2 = 1;
-  for (int q = 0; q < from.ndim; ++q) (q < from.nr ? R1 : C1) *= ext[from.dims[q]];
+  for (int q = from.nr - 1, acc = 1; q >= 0; --q) {
+    sr[from.dims[q]] = acc;
+    acc *= ext[from.dims[q]];
+  }
   for (int q = 0; q < to.ndim; ++q) (q < to.nr ? R2 : C2) *= ext[to.dims[q]];
   const double* sb = src + src_off[src_e[t]];
   double* db = dst + dst_off[t];
   const int ntc1 = tiles8(C1), ntc2 = tiles8(C2);
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    // element offsets per dim from the destination (row, col) of e
-    const int r2 = e / C2, c2 = e - r2 * C2;
-    int o[kMaxRank];
-    int rr = r2, cc = c2;
-    for (int q = to.ndim - 1; q >= to.nr; --q) {
-      const int d = to.dims[q];
-      o[d] = cc % ext[d];
-      cc /= ext[d];
-    }
+  const int64_t slot = static_cast<int64_t>(tiles8(R2)) * ntc2 * 64;
+  auto row_terms = [&](int r2, int& ra, int& ca) {  // dst row -> source row/col terms
+    ra = 0;
+    ca = 0;
     for (int q = to.nr - 1; q >= 0; --q) {
       const int d = to.dims[q];
-      o[d] = rr % ext[d];
-      rr /= ext[d];
+      const int o = r2 % ext[d];
+      r2 /= ext[d];
+      ra += o * sr[d];
+      ca += o * sc[d];
     }
-    int r1 = 0, c1 = 0;
-    for (int q = 0; q < from.nr; ++q) r1 = r1 * ext[from.dims[q]] + o[from.dims[q]];
-    for (int q = from.nr; q < from.ndim; ++q) c1 = c1 * ext[from.dims[q]] + o[from.dims[q]];
-    db[t8_pos(r2, c2, ntc2)] = sb[t8_pos(r1, c1, ntc1)];
+  };
+  auto col_terms = [&](int c2, int& rb, int& cb) {
+    rb = 0;
+    cb = 0;
+    for (int q = to.ndim - 1; q >= to.nr; --q) {
+      const int d = to.dims[q];
+      const int o = c2 % ext[d];
+      c2 /= ext[d];
+      rb += o * sr[d];
+      cb += o * sc[d];
+    }
+  };
+  const bool tables = R2 <= tab_n && C2 <= tab_n;
+  int32_t *RA = tab, *CA = tab + tab_n, *RB = tab + 2 * tab_n, *CB = tab + 3 * tab_n;
+  if (tables) {
+    for (int r = threadIdx.x; r < R2; r += blockDim.x) row_terms(r, RA[r], CA[r]);
+    for (int q = threadIdx.x; q < C2; q += blockDim.x) col_terms(q, RB[q], CB[q]);
+    __syncthreads();
   }
-  (void)R1;
-  (void)R2;
+  // destination tiles in storage order, blockDim / 64 tiles per sweep: lane w
+  // of a 64-thread group always handles element w of its tile (fixed row rr
+  // and swizzled column cc), tile coordinates advance incrementally (32-bit,
+  // no division in the loop)
+  const int ntiles = tiles8(R2) * ntc2;
+  const int w = threadIdx.x & 63;
+  const int rr = w >> 3;
+  const int cc = (w & 7) ^ (((rr >> 1) & 1) << 2);  // the T8 swizzle is an involution
+  const int step = blockDim.x >> 6;
+  int tl = threadIdx.x >> 6;
+  int tr = tl / ntc2, tc = tl - tr * ntc2;
+  for (; tl < ntiles; tl += step) {
+    const int r2 = tr * 8 + rr, c2 = tc * 8 + cc;
+    double v = 0.0;
+    if (r2 < R2 && c2 < C2) {
+      int ra, ca, rb, cb;
+      if (tables) {
+        ra = RA[r2];
+        ca = CA[r2];
+        rb = RB[c2];
+        cb = CB[c2];
+      } else {
+        row_terms(r2, ra, ca);
+        col_terms(c2, rb, cb);
+      }
+      const int r1 = ra + rb, c1 = ca + cb;
+      v = __ldg(sb + (((r1 >> 3) * ntc1 + (c1 >> 3)) << 6) + ((r1 & 7) << 3) +
+                ((c1 & 7) ^ (((r1 >> 1) & 1) << 2)));
+    }
+    db[(static_cast<int64_t>(tl) << 6) + w] = v;
+    tc += step;
+    while (tc >= ntc2) {
+      tc -= ntc2;
+      ++tr;
+    }
+  }
+  (void)slot;
 }
 
 }  // namespace bt
@@ -191,8 +268,8 @@ extern "C" int bt_tensor_remap(bt_ctx* ctx, int ndim, const int64_t* nblocks,
     }
     DBuf<uint64_t> keys(n, st), keys_s(n, st);
     DBuf<int32_t> idx(n, st), idx_s(n, st);
-    k_remap_keys<<<static_cast<unsigned>((S.nbr + 127) / 128), 128, 0, st>>>(
-        S.row_ptr.p, S.col.p, S.nbr, s, from, to, D.nbc, keys.p, idx.p);
+    k_remap_keys<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+        S.row_ptr.p, S.col.p, S.nbr, n, s, from, to, D.nbc, keys.p, idx.p);
     check_launch("remap_keys");
     int end_bit = 1;
     while (end_bit < 64 && (uint64_t(1) << end_bit) < static_cast<uint64_t>(D.nbr * D.nbc)) ++end_bit;
@@ -201,33 +278,39 @@ extern "C" int bt_tensor_remap(bt_ctx* ctx, int ndim, const int64_t* nblocks,
     void* tmp = x.ensure_scratch(bytes);
     cub::DeviceRadixSort::SortPairs(tmp, bytes, keys.p, keys_s.p, idx.p, idx_s.p, n, 0, end_bit, st);
     DBuf<int32_t> cnt(D.nbr + 1, st), rp(D.nbr + 1, st), col(n, st);
+    DBuf<int64_t> len(n + 1, st), el(n + 1, st), d_off(n + 1, st), d_el(n + 1, st);
     BT_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (D.nbr + 1), st));
-    k_remap_rows<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys_s.p, n, D.nbc, cnt.p,
-                                                                         col.p);
-    {
+    k_remap_rows<<<static_cast<unsigned>((n + 256) / 256), 256, 0, st>>>(
+        keys_s.p, n, D.nbc, D.rsz.p, D.csz.p, cnt.p, col.p, len.p, el.p);
+    check_launch("remap_rows");
+    auto scan = [&](auto* in, auto* out, int64_t m) {
       size_t b2 = 0;
-      cub::DeviceScan::ExclusiveSum(nullptr, b2, cnt.p, rp.p, D.nbr + 1, st);
+      cub::DeviceScan::ExclusiveSum(nullptr, b2, in, out, m, st);
       void* t2 = x.ensure_scratch(b2);
-      cub::DeviceScan::ExclusiveSum(t2, b2, cnt.p, rp.p, D.nbr + 1, st);
-    }
-    // destination offsets: host pass over the sorted keys (index-sized work)
-    std::vector<uint64_t> hk(n);
-    BT_CUDA(cudaMemcpyAsync(hk.data(), keys_s.p, 8 * n, cudaMemcpyDeviceToHost, st));
+      cub::DeviceScan::ExclusiveSum(t2, b2, in, out, m, st);
+    };
+    scan(cnt.p, rp.p, D.nbr + 1);
+    scan(len.p, d_off.p, n + 1);   // destination T8 offsets; [n] = slab length
+    scan(el.p, d_el.p, n + 1);     // [n] = stored elements
+    int64_t tot[2];
+    BT_CUDA(cudaMemcpyAsync(&tot[0], d_off.p + n, 8, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaMemcpyAsync(&tot[1], d_el.p + n, 8, cudaMemcpyDeviceToHost, st));
     BT_CUDA(cudaStreamSynchronize(st));
-    std::vector<int64_t> off(n);
-    int64_t nv = 0, ne = 0;
-    for (int64_t t = 0; t < n; ++t) {
-      const int64_t r = static_cast<int64_t>(hk[t] / D.nbc), c = static_cast<int64_t>(hk[t] % D.nbc);
-      off[t] = nv;
-      nv += t8_size(D.h_rsz[r], D.h_csz[c]);
-      ne += int64_t(D.h_rsz[r]) * D.h_csz[c];
-    }
-    DBuf<int64_t> d_off(n, st);
-    BT_CUDA(cudaMemcpyAsync(d_off.p, off.data(), 8 * n, cudaMemcpyHostToDevice, st));
+    const int64_t nv = tot[0], ne = tot[1];
     DBuf<double> vals(std::max<int64_t>(nv, 64), st);
-    BT_CUDA(cudaMemsetAsync(vals.p, 0, 8 * std::max<int64_t>(nv, 64), st));
-    k_remap_vals<<<static_cast<unsigned>(n), 128, 0, st>>>(keys_s.p, idx_s.p, S.off.p, d_off.p, n,
-                                                           D.nbc, s, from, to, S.vals.p, vals.p);
+    // every destination slot is written in full (padding as zeros): no memset
+    // per-block lookup tables sized for the largest destination block of the
+    // launch (from the per-dimension maximum block sizes)
+    int64_t max_r = 1, max_c = 1;
+    for (int q = 0; q < ndim; ++q) {
+      const int d = dst_dims[q];
+      const int32_t mx = nblocks[d] ? *std::max_element(dim_sizes[d], dim_sizes[d] + nblocks[d]) : 1;
+      (q < dst_nrow ? max_r : max_c) *= mx;
+    }
+    const int64_t tab_want = std::max(max_r, max_c);
+    const int tab_n = tab_want <= kRemapTabMax ? static_cast<int>(tab_want) : 0;
+    k_remap_vals<<<static_cast<unsigned>(n), 128, 16 * static_cast<size_t>(tab_n), st>>>(
+        keys_s.p, idx_s.p, S.off.p, d_off.p, n, D.nbc, s, from, to, S.vals.p, vals.p, tab_n);
     check_launch("remap_vals");
     count_launch(&x, 8);
     D.vals = std::move(vals);

@@ -30,7 +30,7 @@ def test_nccl_drivers(world, force_miss):
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     print(p.stdout[-4000:])
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
-    assert p.stdout.count(": OK") >= 6
+    assert p.stdout.count(": OK") >= 8
 
 
 @pytest.mark.parametrize("world", [2, 4])
