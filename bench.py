@@ -216,8 +216,9 @@ def relaunch_under_torchrun(n: int):
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if env.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        env["NCCL_DEBUG"] = "INFO"          # the communicator init lines (ranks, NVLink)
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.abspath(__file__)] + sys.argv[1:]
