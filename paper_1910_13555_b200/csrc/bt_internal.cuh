@@ -37,6 +37,26 @@ void set_last_error(const std::string& msg);
     if (!(cond)) throw ::bt::Error((code), (msg)); \
   } while (0)
 
+// Device-side invariant checks, compiled in only for the checked build
+// (make checked -> libbtcuda_checked.so, -DBT_DEVICE_CHECKS): out-of-range slab
+// offsets, descriptor / work-item indices and a bounded spin on the K-panel
+// flags trap with a message.  This pool has compute-sanitizer closed, so the
+// parity suite run against the checked build is the bounds / race evidence.
+#ifdef BT_DEVICE_CHECKS
+#define BT_DASSERT(cond, what)                                                         \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("BT_DASSERT failed: %s (%s:%d) block %d thread %d\n", what, __FILE__,      \
+             __LINE__, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));   \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define BT_DASSERT(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 // wraps a C-ABI body: converts exceptions to status codes + bt_last_error()
 template <class F>
 int guard(F&& f) {

@@ -98,6 +98,7 @@ struct RowArgs {
   // work items, written by the fill pass into per-class segments
   unsigned long long* class_cursor;  // [NSEG], initialised to the segment bases
   Item* items;
+  int64_t nprod_total, nitems_total;  // device checks of the checked build
 };
 
 __device__ __forceinline__ int band_of(int64_t j, const RowArgs& g) {
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         if (j == 0xffffffffu) continue;
         const int l = find_entry(rc, n, static_cast<int32_t>(t));
         const int32_t p = cur[j] + __popcll(mask[j] & ((1ull << l) - 1ull));
+        BT_DASSERT(p >= 0 && pbase + p < g.prod_base[i + 1], "descriptor slot");
         g.desc[pbase + p] = make_int4(rc.au[l], s_bu[t], (rc.ksz[l] + 3) >> 2, rc.k[l]);
       }
       __syncthreads();
@@ -515,6 +517,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
         const int32_t j = static_cast<int32_t>(g.b_col[f] - j0);
         const int32_t p = cur[j] + __popcll(mask[j] & ((1ull << l) - 1ull));
+        BT_DASSERT(p >= 0 && pbase + p < g.prod_base[i + 1], "descriptor slot");
         g.desc[pbase + p] = make_int4(rc.au[l], static_cast<int32_t>(g.b_off[f] >> 6),
                                       (rc.ksz[l] + 3) >> 2, rc.k[l]);
       }
@@ -554,7 +557,8 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
             const uint32_t j = s_key[t - w0];
             if (j == 0xffffffffu) continue;
             const int32_t p = cur[j]++;  // one pair per column per k: race free
-            g.desc[pbase + p] = make_int4(au, s_bu[t - w0], kc, rc.k[l]);
+            BT_DASSERT(p >= 0 && pbase + p < g.prod_base[i + 1], "descriptor slot");
+        g.desc[pbase + p] = make_int4(au, s_bu[t - w0], kc, rc.k[l]);
           }
           __syncthreads();
         }
@@ -599,6 +603,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         const int l = s_l[slot];
         const int kc = (rc.ksz[l] + 3) >> 2;
         const int32_t p = cur[jkey] + (q - lo);
+        BT_DASSERT(p >= 0 && pbase + p < g.prod_base[i + 1], "descriptor slot");
         g.desc[pbase + p] = make_int4(rc.au[l], s_bu[slot], kc, rc.k[l]);
       }
       __syncthreads();
@@ -649,6 +654,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
       it.np = g.out_np[c];
       it.rows = static_cast<int16_t>(nt > 1 ? min(g.tall_rows, m - r0) : m);
       it.n = static_cast<int16_t>(n);
+      BT_DASSERT(static_cast<int64_t>(at) + q < g.nitems_total, "work item slot");
       g.items[at + q] = it;
     }
   }
@@ -1135,6 +1141,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     Item* items = x.ws<Item>(17, nitems);
     ra.class_cursor = cursor;
     ra.items = items;
+    ra.nprod_total = nprod;
+    ra.nitems_total = nitems;
     if (phases) BT_CUDA(cudaEventRecord(x.ev[5], st));
     if (nout > 0) {
       ensure_dyn_smem(reinterpret_cast<const void*>(k_row_fill), row_smem);
@@ -1160,6 +1168,10 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       g.bt = B.vals.p;
       g.cin = Cm.vals.p;
       g.cout = new_vals.p;
+      g.a_len = A.nvals;
+      g.b_len = B.nvals;
+      g.cin_len = Cm.nvals;
+      g.cout_len = nvals;
       unsigned long long* counters = cursor + NSEG;
       // K panels: when the operands are far larger than L2, C is comparatively
       // small and product chains are long (the case-1 regime: S_C << S_A, S_B),

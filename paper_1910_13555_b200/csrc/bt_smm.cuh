@@ -58,6 +58,8 @@ struct NumArgs {
   int npanels;
   int64_t panel_stride;
   int* tile_flag;
+  // slab lengths in doubles (device checks of the checked build)
+  int64_t a_len, b_len, cin_len, cout_len;
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -261,6 +263,10 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         double* st = stages + static_cast<int64_t>(s) * g.stage_doubles;
         stage_kc[s] = d.z;
         fence_proxy_async_smem();
+        BT_DASSERT((static_cast<int64_t>(d.x) + static_cast<int64_t>(p_r8) * KT) * 64 + ba / 8 <=
+                       g.a_len, "A slab range");
+        BT_DASSERT(static_cast<int64_t>(d.y) * 64 + bb / 8 <= g.b_len, "B slab range");
+        BT_DASSERT(ba + bb <= static_cast<uint32_t>(g.stage_doubles) * 8u, "stage capacity");
         mbar_arrive_expect_tx(&bars[s], ba + bb);
         // (an L2 evict_last hint on these copies measured neutral on c1/c3)
         bulk_g2s(st, g.at + (static_cast<int64_t>(d.x) + static_cast<int64_t>(p_r8) * KT) * 64,
@@ -286,8 +292,14 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
       panel = static_cast<int>(tick / g.nitems);
       flag = g.tile_flag + (tick - static_cast<int64_t>(panel) * g.nitems);
       if (panel > 0) {
-        if (lane == 0)
-          while (ld_acquire_gpu(flag) < panel) __nanosleep(32);
+        if (lane == 0) {
+          long long spins = 0;
+          while (ld_acquire_gpu(flag) < panel) {
+            __nanosleep(32);
+            BT_DASSERT(++spins < (1ll << 28), "K-panel flag wait (deadlock)");
+          }
+          (void)spins;
+        }
         __syncwarp();
       }
     }
@@ -375,6 +387,11 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         top_up();
       }
       double* dst = g.cout + it.c_off;
+      BT_DASSERT(it.c_off >= 0 && it.c_off + static_cast<int64_t>(mt) * CN * 64 <= g.cout_len,
+                 "C tile range");
+      BT_DASSERT(it.cin_off < 0 || it.cin_off + static_cast<int64_t>(mt) * CN * 64 <=
+                                       (cin == g.cout ? g.cout_len : g.cin_len),
+                 "C_in tile range");
 #pragma unroll
       for (int tm = 0; tm < CM; ++tm)
         if (tm < mt) {
@@ -430,6 +447,7 @@ __global__ void k_smm_generic(const NumArgs g) {
   for (int e = threadIdx.x; e < padded; e += blockDim.x) {
     const int r = e / (NT * 8), q = e - r * (NT * 8);
     const int64_t cp = t8_pos(r, q, NT);
+    BT_DASSERT(it.c_off + cp < g.cout_len, "generic C range");
     if (r >= m || q >= n) {
       g.cout[it.c_off + cp] = 0.0;
       continue;

@@ -150,7 +150,14 @@ class LocalStore:
         if vals_out is None:
             vals = np.zeros(ne, np.float64)
             vp = ptr(vals, _f64p)
-        else:
+        elif isinstance(vals_out, np.ndarray):
+            if vals_out.dtype != np.float64 or not vals_out.flags.c_contiguous or vals_out.size < ne:
+                from ._lib import InvalidArgument
+                raise InvalidArgument("export: output must be a contiguous float64 array of "
+                                      f"at least {ne} elements")
+            vals = vals_out
+            vp = ptr(vals_out, _f64p)
+        else:  # torch tensor (e.g. pinned)
             vals = vals_out
             vp = C.cast(C.c_void_p(vals_out.data_ptr()), _f64p)
         fn = self.lib.bt_mat_export_async if asynchronous else self.lib.bt_mat_export
