@@ -32,7 +32,10 @@ int env_int(const char* name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 
-enum { NCLASS = 17, GENERIC = 16 };
+// DMMA tile classes 0..15, GENERIC (n > 32 or k > 64), TINY (m, n <= 5: the
+// CUDA-core DFMA kernel)
+enum { NCLASS = 18, GENERIC = 16, TINY = 17 };
+constexpr int kTinyMax = 5;
 // Work-item segments: (tile class, column band).  Within a class the bands are
 // consecutive, band-major, so the numeric phase sweeps C in column bands and
 // only B(:, band) has to stay resident in L2.
@@ -43,14 +46,15 @@ constexpr uint32_t kCinFlag = 0x80000000u;
 // Tile classes: 16 DMMA tile shapes (ceil(m/8) in 1..4 -- blocks taller than
 // `tr` rows (24 or 32) are cut in tr-row tiles -- times ceil(n/8) in 1..4) +
 // GENERIC (n > 32 or k > 64).
-__host__ __device__ inline int shape_class(int m, int n, bool dmma_ok, int tr) {
+__host__ __device__ inline int shape_class(int m, int n, bool dmma_ok, int tr, bool tiny) {
+  if (tiny && m <= kTinyMax && n <= kTinyMax) return TINY;
   if (!dmma_ok || n > 32) return GENERIC;
   const int mc = m > tr ? tr / 8 : (m + 7) / 8;
   const int nc = (n + 7) / 8;
   return (mc - 1) * 4 + (nc - 1);
 }
 __host__ __device__ inline int class_tiles(int m, int cls, int tr) {
-  return (cls != GENERIC && m > tr) ? (m + tr - 1) / tr : 1;
+  return (cls < GENERIC && m > tr) ? (m + tr - 1) / tr : 1;
 }
 
 __device__ __forceinline__ bool keep_product(const double* na, const double* nb, int32_t e,
@@ -72,6 +76,7 @@ struct RowArgs {
   int sort_min;   // rows with more A entries per chunk emit by window sort
   bool colmask;   // k_row_fill has a 64-bit per-column mask array (N <= kMaskCols)
   int tall_rows;  // tile height for blocks taller than 32 rows (24 or 32)
+  bool tiny;      // m, n <= kTinyMax C blocks go to the DFMA kernel (class TINY)
   // column chunk width of the symbolic passes: rows are processed in chunks
   // of `colw` block columns (per-column counters in shared memory are sized
   // for one chunk), so C may have any number of block columns
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
       prods += v & ~kCinFlag;
       vals += t8_size(m, n);
       elems += static_cast<long long>(m) * n;
-      const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
+      const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
       const int seg = cls * kMaxBands + band_of(j, g);
       agg_add(&cls_items[seg], seg,
               static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
@@ -445,7 +450,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
         g.out_p0[c] = pbase + run_prod + p_ex;
         cur[j] = static_cast<int32_t>(run_prod + p_ex);
         cnt[j] = static_cast<uint32_t>(run_q + q);  // rank of the C entry in the row
-        const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
+        const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
         const int seg = cls * kMaxBands + band_of(jg, g);
         agg_add(&cls_n[seg], seg,
                 static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
@@ -639,7 +644,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
   for (int32_t c = cbase + threadIdx.x; c < g.out_rp[i + 1]; c += blockDim.x) {
     const int j = g.out_col[c];
     const int n = g.n_sz[j];
-    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows);
+    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
     const int nt = class_tiles(m, cls, g.tall_rows);
     const int seg = cls * kMaxBands + band_of(j, g);
     const unsigned long long at = agg_add(&cls_at[seg], seg, static_cast<unsigned long long>(nt));
@@ -1017,6 +1022,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.sort_min = env_int("BT_SORT_MIN", 48);
     ra.colmask = colmask;
     ra.tall_rows = env_int("BT_TALL_ROWS", 32) == 24 ? 24 : 32;
+    ra.tiny = env_int("BT_DFMA", 1) != 0;
     ra.splits = fill_splits;
     ra.colw = colw;
     {
@@ -1186,7 +1192,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         // at 64); several classes: one launch per panel, fewer and larger
         int present = 0;
         for (int q = 0; q < NCLASS; ++q) present += ibound[q + 1] > ibound[q];
-        const bool one = present == 1 && ibound[GENERIC + 1] == ibound[GENERIC];
+        const bool one = present == 1 && ibound[GENERIC] > ibound[0];
         const double per_tile = static_cast<double>(nprod) / static_cast<double>(nitems);
         int p = static_cast<int>(std::ceil(ab_bytes / (one ? 100e6 : 60e6)));
         p = std::min(p, static_cast<int>(per_tile / 4));          // >= ~4 products/panel
@@ -1224,7 +1230,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
           only = q;
           ++present;
         }
-      const bool fused = npanels > 1 && present == 1 && only != GENERIC &&
+      const bool fused = npanels > 1 && present == 1 && only < GENERIC &&
                          env_int("BT_PANEL_FUSE", 1) != 0;
       if (fused) {
         const int q = only;
@@ -1299,7 +1305,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       for (int q = 0; q < NCLASS; ++q) {
         const int64_t lo = ibound[q], hi = ibound[q + 1];
         if (hi <= lo) continue;
-        if (multi && q != GENERIC) continue;
+        if (multi && q < GENERIC) continue;  // (the MULTI launch covers every DMMA class)
         cudaStream_t ks = fork ? x.aux[launched % nstreams] : st;
         ++launched;
         g.item_lo = lo;
@@ -1308,6 +1314,14 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         if (q == GENERIC) {
           k_smm_generic<<<static_cast<unsigned>(hi - lo), 128, 0, ks>>>(g);
           check_launch("smm_generic");
+          count_launch(&x);
+          continue;
+        }
+        if (q == TINY) {  // CUDA-core DFMA, one thread per C block
+          const bool four = A.max_r <= 4 && B.max_c <= 4;
+          (four ? k_smm_dfma<4, 4> : k_smm_dfma<kTinyMax, kTinyMax>)
+              <<<blocks_for(hi - lo, 128), 128, 0, ks>>>(g, A.csz.p);
+          check_launch("smm_dfma");
           count_launch(&x);
           continue;
         }

@@ -431,6 +431,82 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
   }
 }
 
+// ---------------------------------------------------------------------------
+// CUDA-core FP64 FMA (DFMA) small-GEMM for tiny C blocks (m, n <= 5): the
+// shapes that do not tile onto the 8x8 DMMA fragment -- a 5x5x5 product uses
+// 24 % of an 8x8x8 DMMA tile, 4x4x4 12.5 %, 1x1x1 0.2 %.  One THREAD owns one
+// C block for its whole product chain: the MM x NN accumulators stay in
+// registers, every k step is one B row (NN doubles from the T8 tile row, the
+// XOR swizzle undone in registers) and MM A elements, MM*NN DFMAs, over the
+// exact k of each product (no k padding work).  Products in ascending k per C
+// block (block.hpp:45-60 order); the whole 8x8 T8 slot is written (padding 0).
+// A warp works 32 C blocks at once, so its loads of 32 independent blocks
+// are in flight together (memory-level parallelism without a staging ring).
+template <int MM, int NN>
+__global__ void __launch_bounds__(128) k_smm_dfma(const NumArgs g, const int32_t* __restrict__ k_sz) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= g.nitems) return;
+  const Item it = g.items[g.item_lo + t];
+  const int m = it.rows, n = it.n;
+  const double* cin = g.cin;  // later K panels: the host passes C_out (in place)
+  double acc[MM][NN];
+#pragma unroll
+  for (int r = 0; r < MM; ++r)
+#pragma unroll
+    for (int c = 0; c < NN; ++c) {
+      double v = 0.0;
+      if (it.cin_off >= 0 && r < m && c < n) v = cin[it.cin_off + r * 8 + (c ^ (((r >> 1) & 1) << 2))];
+      acc[r][c] = v;
+    }
+  const int64_t p0 = item_p0(it);
+  for (int p = 0; p < it.np; ++p) {
+    const Desc d = g.desc[p0 + p];
+    const int k = k_sz[d.w];
+    const int KT = (d.z + 1) >> 1;
+    const double* A = g.at + static_cast<int64_t>(d.x) * 64;
+    const double* B = g.bt + static_cast<int64_t>(d.y) * 64;
+    BT_DASSERT(static_cast<int64_t>(d.x) * 64 + static_cast<int64_t>(KT) * 64 <= g.a_len,
+               "dfma A range");
+    BT_DASSERT(static_cast<int64_t>(d.y) * 64 + static_cast<int64_t>(KT) * 64 <= g.b_len,
+               "dfma B range");
+    (void)KT;
+    for (int kk = 0; kk < k; ++kk) {
+      // B row kk (NT = 1: one tile column): 8 doubles of tile row kk & 7 of
+      // k tile kk >> 3, stored with column u at u ^ sw
+      const double* brow = B + ((kk >> 3) << 6) + ((kk & 7) << 3);
+      const int sw = ((kk >> 1) & 1) << 2;
+      double b[NN];
+#pragma unroll
+      for (int c = 0; c < NN; ++c) b[c] = c < n ? __ldg(brow + (c ^ sw)) : 0.0;
+      // A column kk: element (r, kk) of the m x k block, k tile kk >> 3 of the
+      // block's first (only) 8-row tile row
+      const double* acol = A + ((kk >> 3) << 6);
+#pragma unroll
+      for (int r = 0; r < MM; ++r)
+        if (r < m) {
+          const double a = __ldg(acol + r * 8 + ((kk & 7) ^ (((r >> 1) & 1) << 2)));
+#pragma unroll
+          for (int c = 0; c < NN; ++c) acc[r][c] = fma(a, b[c], acc[r][c]);
+        }
+    }
+  }
+  // the full 8x8 slot, rows as 16-byte pairs; padding rows / columns zero
+  double* dst = g.cout + it.c_off;
+  BT_DASSERT(it.c_off >= 0 && it.c_off + 64 <= g.cout_len, "dfma C range");
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    double row[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) row[u] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NN; ++c)
+      if (r < MM && r < m && c < n) row[c ^ (((r >> 1) & 1) << 2)] = acc[r < MM ? r : 0][c];
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      __stcs(reinterpret_cast<double2*>(dst + r * 8 + 2 * h), make_double2(row[2 * h], row[2 * h + 1]));
+  }
+}
+
 // Generic small-GEMM (n > 32 or k > 64): one CTA per C block, one thread per
 // element, T8 operands, products in k order.  Every position of the T8 slot is
 // written -- the padding with zeros -- because the output slab is not cleared

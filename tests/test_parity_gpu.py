@@ -400,3 +400,45 @@ def test_column_chunks(oracle, ctx, monkeypatch, colw, colmask, sort_min, splits
             out[(w, eps)] = got
     for eps in (0.0, 30.0):
         assert np.array_equal(out[(str(colw), eps)].vals, out[("1000000", eps)].vals)
+
+
+@pytest.mark.parametrize("case", ["tiny_uniform", "tiny_mixed_k", "tiny_with_dmma", "panels",
+                                  "cin_eps"])
+def test_dfma_tiny_blocks(oracle, ctx, monkeypatch, case):
+    """C blocks with m, n <= 5 on the CUDA-core DFMA kernel (k_smm_dfma, one
+    thread per C block) against the oracle, and against the DMMA path
+    (BT_DFMA=0); mixed with DMMA classes in one multiply, K panels, C_in and
+    the eps filter."""
+    from paper_1910_13555_b200.store import multiply_local
+    rng = np.random.default_rng(88)
+    eps = 0.0
+    if case == "tiny_uniform":
+        sz = np.array([1, 2, 3, 4], np.int32)[rng.integers(0, 4, 60)]
+        A, B, Cin = _case(oracle, 1600, sz, sz, sz, 0.3, 0.3, 0.0)
+    elif case == "tiny_mixed_k":
+        ms = np.array([5, 3, 1], np.int32)[rng.integers(0, 3, 30)]
+        ks = np.array([5, 13, 23, 40, 70], np.int32)[rng.integers(0, 5, 40)]
+        A, B, Cin = _case(oracle, 1700, ms, ks, ms, 0.3, 0.3, 0.1)
+    elif case == "tiny_with_dmma":
+        sz = np.array([5, 13, 23, 4, 8], np.int32)[rng.integers(0, 5, 50)]
+        A, B, Cin = _case(oracle, 1800, sz, sz, sz, 0.2, 0.2, 0.1)
+    elif case == "panels":
+        monkeypatch.setenv("BT_KPANELS", "3")
+        ms = np.array([5, 4, 13], np.int32)[rng.integers(0, 3, 20)]
+        ks = np.array([5, 23], np.int32)[rng.integers(0, 2, 80)]
+        A, B, Cin = _case(oracle, 1900, ms, ks, ms, 0.2, 0.2, 0.2)
+    else:
+        sz = np.array([5, 3, 13], np.int32)[rng.integers(0, 3, 50)]
+        A = oracle.random_matrix(2000, sz, sz, 0.3, 6.0)
+        B = oracle.random_matrix(2001, sz, sz, 0.3, 6.0)
+        Cin = oracle.random_matrix(2002, sz, sz, 0.2, 6.0)
+        eps = 1e-4
+    want, nprod, _ = oracle.multiply(A, B, Cin, eps)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BT_DFMA", mode)
+        a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+        st = multiply_local(ctx, a, b, c, eps)
+        assert st["products"] == nprod
+        assert_parity(from_store(c), want)
+        # the DFMA output slots carry zero padding (norms read it)
+        assert np.allclose(c.norms(), oracle.norms(want), rtol=1e-12, atol=0)

@@ -61,6 +61,16 @@ def config(name, rng, occ=None):
         M = blocks_random(rng, aux, aux, 0.0, band=7)
         return rows, aux, aux, T, M, 0.0, ("c4: (ab|P)(P|Q), a,b 200 AO blocks, P,Q 400 aux "
                                            "blocks, 13/23 alternating, T occ 0.001, (P|Q) band 7")
+    if name in ("tiny5", "tiny3", "tiny1"):
+        # not a BASELINE config: uniform tiny blocks, ~20 products per C block
+        # (compute-heavy), the DFMA-vs-DMMA A/B workload (BT_DFMA=0/1)
+        bs = int(name[4:])
+        nb = {5: 2000, 3: 2400, 1: 4000}[bs]
+        o = {5: 0.01, 3: 0.01, 1: 0.005}[bs] if occ is None else occ
+        sz = np.full(nb, bs, np.int32)
+        A = blocks_random(rng, sz, sz, o)
+        B = blocks_random(rng, sz, sz, o)
+        return sz, sz, sz, A, B, 0.0, (f"{name}: {nb}x{nb} blocks of {bs}x{bs}, occ {o}")
     raise SystemExit(f"unknown config {name}")
 
 
