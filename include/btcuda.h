@@ -153,6 +153,11 @@ int bt_grid_info(const bt_grid* g, int* nranks, int* first_local, int* nlocal);
  * 2 meta sent, 3 meta received; phase NULL/"" = rank total. */
 int bt_grid_ledger(const bt_grid* g, int rank, const char* phase, int what, int64_t* out);
 int bt_grid_reset_ledger(bt_grid* g);
+/* Sum of n int64 values over the processes of the group (every process passes
+ * its local partial; all receive the total).  A no-op for virtual ranks (one
+ * process holds every rank).  Used for global counts such as the stored
+ * elements behind measured_spec (multiply_rect.hpp:254-265) in NCCL mode. */
+int bt_grid_sum(bt_grid* g, int64_t* values, int n);
 
 /* new_matrix (matrix.hpp:404-410): blockings + ProcessGrid dims + Axis
  * distributions; NULL distributions = round robin (new_matrix_round_robin,

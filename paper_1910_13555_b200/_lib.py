@@ -100,6 +100,7 @@ SIGNATURES = {
                                C.POINTER(C.c_int)]),
     "bt_grid_ledger": (C.c_int, [C.c_void_p, C.c_int, C.c_char_p, C.c_int, _i64p]),
     "bt_grid_reset_ledger": (C.c_int, [C.c_void_p]),
+    "bt_grid_sum": (C.c_int, [C.c_void_p, _i64p, C.c_int]),
     "bt_dmat_create": (C.c_int, [C.c_void_p, C.c_int64, _i32p, C.c_int64, _i32p, C.c_int,
                                  C.c_int, _i32p, _i32p, C.POINTER(C.c_void_p)]),
     "bt_dmat_destroy": (C.c_int, [C.c_void_p]),

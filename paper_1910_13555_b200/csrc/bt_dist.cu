@@ -1533,6 +1533,22 @@ int bt_grid_info(const bt_grid* g, int* nranks, int* first_local, int* nlocal) {
   });
 }
 
+int bt_grid_sum(bt_grid* g, int64_t* values, int n) {
+  return guard([&] {
+    BT_REQUIRE(g && (values || n == 0) && n >= 0, BT_ERR_INVALID_ARGUMENT, "null argument");
+    Grid& G = g->impl;
+    if (!G.nccl || n == 0) return;  // one process holds every rank: nothing to add
+    Ctx& x = *G.ctx;
+    int64_t* d = x.ws<int64_t>(14, n);
+    BT_CUDA(cudaMemcpyAsync(d, values, 8 * n, cudaMemcpyHostToDevice, x.stream));
+    const ncclResult_t r = ncclAllReduce(d, d, n, ncclInt64, ncclSum,
+                                         static_cast<ncclComm_t>(x.nccl), x.stream);
+    BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    BT_CUDA(cudaMemcpyAsync(values, d, 8 * n, cudaMemcpyDeviceToHost, x.stream));
+    BT_CUDA(cudaStreamSynchronize(x.stream));
+  });
+}
+
 int bt_grid_ledger(const bt_grid* g, int rank, const char* phase, int what, int64_t* out) {
   return guard([&] {
     BT_REQUIRE(g && out, BT_ERR_INVALID_ARGUMENT, "null argument");

@@ -351,7 +351,13 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
 // Pairs of up to kPairCap are staged in shared memory by all threads in
 // parallel; the ordered emission then walks the staged A entries one k at a
 // time touching shared memory only.
-__global__ void __launch_bounds__(kChunkA) k_row_fill(const RowArgs g) {
+// 4 resident CTAs per SM (64 registers, no spills): the fill is latency bound
+// -- measured fill 50.8 -> 38.7 us (c1), 53 -> 45 (c2), 540 -> 318 (c4)
+// against the unconstrained 111-register build (profiles/r02/fill_occupancy_ab.txt)
+#ifndef BT_FILL_MINB
+#define BT_FILL_MINB 4
+#endif
+__global__ void __launch_bounds__(kChunkA, BT_FILL_MINB) k_row_fill(const RowArgs g) {
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                                        // counts -> C entry rank
   int32_t* cur = reinterpret_cast<int32_t*>(sm + g.colw);  // product cursor

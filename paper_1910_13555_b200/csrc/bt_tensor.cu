@@ -177,31 +177,39 @@ __global__ void __launch_bounds__(128) k_remap_vals(
   const int rr = w >> 3;
   const int cc = (w & 7) ^ (((rr >> 1) & 1) << 2);  // the T8 swizzle is an involution
   const int step = blockDim.x >> 6;
-  int tl = threadIdx.x >> 6;
-  int tr = tl / ntc2, tc = tl - tr * ntc2;
-  for (; tl < ntiles; tl += step) {
-    const int r2 = tr * 8 + rr, c2 = tc * 8 + cc;
-    double v = 0.0;
-    if (r2 < R2 && c2 < C2) {
-      int ra, ca, rb, cb;
-      if (tables) {
-        ra = RA[r2];
-        ca = CA[r2];
-        rb = RB[c2];
-        cb = CB[c2];
-      } else {
-        row_terms(r2, ra, ca);
-        col_terms(c2, rb, cb);
+  // four tiles per thread and sweep: the four gathers are issued together
+  // (the kernel is bound by gather latency, ncu: long-scoreboard stalls)
+  constexpr int U = 4;
+  for (int t0 = threadIdx.x >> 6; t0 < ntiles; t0 += U * step) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tl = t0 + u * step;
+      v[u] = 0.0;
+      if (tl < ntiles) {
+        const int tr = tl / ntc2, tc = tl - tr * ntc2;
+        const int r2 = tr * 8 + rr, c2 = tc * 8 + cc;
+        if (r2 < R2 && c2 < C2) {
+          int ra, ca, rb, cb;
+          if (tables) {
+            ra = RA[r2];
+            ca = CA[r2];
+            rb = RB[c2];
+            cb = CB[c2];
+          } else {
+            row_terms(r2, ra, ca);
+            col_terms(c2, rb, cb);
+          }
+          const int r1 = ra + rb, c1 = ca + cb;
+          v[u] = __ldg(sb + (((r1 >> 3) * ntc1 + (c1 >> 3)) << 6) + ((r1 & 7) << 3) +
+                       ((c1 & 7) ^ (((r1 >> 1) & 1) << 2)));
+        }
       }
-      const int r1 = ra + rb, c1 = ca + cb;
-      v = __ldg(sb + (((r1 >> 3) * ntc1 + (c1 >> 3)) << 6) + ((r1 & 7) << 3) +
-                ((c1 & 7) ^ (((r1 >> 1) & 1) << 2)));
     }
-    db[(static_cast<int64_t>(tl) << 6) + w] = v;
-    tc += step;
-    while (tc >= ntc2) {
-      tc -= ntc2;
-      ++tr;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int tl = t0 + u * step;
+      if (tl < ntiles) __stcs(db + (static_cast<int64_t>(tl) << 6) + w, v[u]);
     }
   }
   (void)slot;

@@ -408,11 +408,22 @@ class DistMatrix:
         out = np.concatenate([vals[off[t]:off[t + 1]] for t in order]) if len(order) else vals
         return bi[order], bj[order], out
 
+    def _global_counts(self):
+        """(blocks, elements) stored over ALL ranks (matrix.hpp stored_* are
+        global); with one process per GPU this is a collective over the group
+        (bt_grid_sum) -- every process must call it."""
+        v = np.zeros(2, np.int64)
+        for r in self.comm.local_ranks():
+            if r < self.nranks():
+                v += np.array(self.local(r).info(), np.int64)
+        check(self.comm.lib.bt_grid_sum(self.comm.g, ptr(v, _i64p), 2), "grid_sum")
+        return int(v[0]), int(v[1])
+
     def stored_blocks(self):
-        return sum(self.local(r).info()[0] for r in self.comm.local_ranks() if r < self.nranks())
+        return self._global_counts()[0]
 
     def stored_elements(self):
-        return sum(self.local(r).info()[1] for r in self.comm.local_ranks() if r < self.nranks())
+        return self._global_counts()[1]
 
     def occupancy(self):
         dense = self._rows.total() * self._cols.total()
@@ -488,15 +499,51 @@ def multiply_virtual_case2(comm, a, b, c, nprocs, eps=0.0, gather=False) -> dict
 
 
 class Algorithm:
-    cannon, case1, case2 = 0, 1, 2
+    cannon, case1, case2, auto = 0, 1, 2, 3
 
 
 def algorithm_name(a):
-    return {0: "cannon", 1: "case1", 2: "case2"}.get(a, "?")
+    return {0: "cannon", 1: "case1", 2: "case2", 3: "auto"}.get(a, "?")
+
+
+def cannon_ready(a, b, c, nprocs) -> bool:
+    """Cannon's layout preconditions (multiply_cannon.hpp:65-78): a square grid
+    of nprocs ranks, C distributed as A's rows x B's columns."""
+    g = a.grid()
+    q = g.dim(0)
+    return (g.dim(0) == g.dim(1) and q * q == nprocs and b.grid() == g and c.grid() == g
+            and np.array_equal(c.row_dist(), a.row_dist())
+            and np.array_equal(c.col_dist(), b.col_dist())
+            and np.array_equal(a.col_dist(), b.row_dist()))
+
+
+def select_for(a, b, c, nprocs, machine=None):
+    """The B200 selection for these operands: measured occupancies (a
+    collective with one process per GPU), C's occupancy estimated from them
+    (multiply_rect.hpp:84-88), argmin of predicted_time_b200 over the
+    algorithms whose preconditions hold."""
+    s = measured_spec(a, b, 0.0, nprocs)
+    s.occ_c = estimate_result_occupancy(s.occ_a, s.occ_b, a.n_block_cols())
+    machine = machine or B200Machine()
+    cands = ([Algorithm.cannon] if cannon_ready(a, b, c, nprocs) else []) + \
+        [Algorithm.case1, Algorithm.case2]
+    times = {al: predicted_time_b200(al, s, machine) for al in cands}
+    return min(cands, key=lambda al: (times[al], al)), times
 
 
 def multiply_dispatch(comm, algo, a, b, c, nprocs, eps=0.0) -> dict:
-    """multiply_rect.hpp:242-250."""
+    """multiply_rect.hpp:242-250; Algorithm.auto picks the algorithm with the
+    NVLink-aware time model (select_for) and runs case 2 in its
+    one-step NVLink gather form."""
+    if algo == Algorithm.auto:
+        algo, _ = select_for(a, b, c, nprocs)
+        if algo == Algorithm.case2:
+            st = multiply_virtual_case2(comm, a, b, c, nprocs, eps, gather=True)
+            st["algorithm"] = "case2"
+            return st
+        st = multiply_dispatch(comm, algo, a, b, c, nprocs, eps)
+        st["algorithm"] = algorithm_name(algo)
+        return st
     if algo == Algorithm.cannon:
         return multiply_cannon(comm, a, b, c, eps)
     if algo == Algorithm.case1:

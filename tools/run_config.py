@@ -38,6 +38,11 @@ def blocks_random(rng, rsz, csz, occ, scale_exp=0.0, band=None):
 
 def config(name, rng, occ=None):
     """returns (rsz, ksz, nsz, A, B, eps, description)"""
+    if name == "c1":
+        sz = np.full(400, 23, np.int32)
+        A = blocks_random(rng, sz, sz, 0.10)
+        B = blocks_random(rng, sz, sz, 0.10)
+        return sz, sz, sz, A, B, 0.0, "c1: 400x400 blocks of 23x23, occ 0.10 (bench.py's workload shape)"
     if name == "c2":
         sizes = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 1463)]
         A = blocks_random(rng, sizes, sizes, 0.01, 12.0)
