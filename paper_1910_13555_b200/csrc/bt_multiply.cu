@@ -284,6 +284,16 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
   __shared__ unsigned long long cls_items[NSEG];
   __shared__ RowChunk rc;
   const int64_t i = blockIdx.x;
+  // empty C row (no A entries, no C_in blocks): sizes are zero, nothing else
+  // (tensor-shaped operands such as c4 leave most matricized rows empty)
+  if (g.a_rp[i] == g.a_rp[i + 1] && g.c_rp[i] == g.c_rp[i + 1]) {
+    if (threadIdx.x == 0) {
+      g.row_nnz[i] = 0;
+      g.row_prod[i] = 0;
+      g.row_vals[i] = 0;
+    }
+    return;
+  }
   for (int t = threadIdx.x; t < NSEG; t += blockDim.x) cls_items[t] = 0;
   unsigned long long cand = 0, mnk = 0;
   const int m = g.m_sz[i];
@@ -374,6 +384,7 @@ __global__ void __launch_bounds__(kChunkA, BT_FILL_MINB) k_row_fill(const RowArg
   // the row's C index and work items are written by CTA 0
   const int64_t i = blockIdx.x / g.splits;
   const int split = static_cast<int>(blockIdx.x % g.splits);
+  if (g.out_rp[i] == g.out_rp[i + 1]) return;  // empty C row: nothing to emit
   const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
   const int nch = (a1 - a0 + kChunkA - 1) / kChunkA;
   const int ch_lo = static_cast<int>((static_cast<int64_t>(split) * nch) / g.splits);
