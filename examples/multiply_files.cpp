@@ -1,7 +1,7 @@
 // multiply_files.cpp -- a caller written against the reference API, compiled
 // against the B200 facade instead (include/blocktensor/b200.hpp).
 //
-//   multiply_files <cannon|case1|case2> <grid q> <nprocs> A B C Cout [text|binary]
+//   multiply_files <cannon|case1|case2|auto> <grid q> <nprocs> A B C Cout [text|binary]
 //
 // Fixtures in the reference's formats (io.hpp:22-198, default binary).
 // One process: every rank is a virtual rank on this process's GPU.  Under
@@ -65,9 +65,14 @@ int main(int argc, char** argv) {
     DistMatrix a = to_dist_matrix(read_matrix_file(argv[4], fmt), grid);
     DistMatrix b = to_dist_matrix(read_matrix_file(argv[5], fmt), grid);
     DistMatrix c = to_dist_matrix(read_matrix_file(argv[6], fmt), grid);
-    const Algorithm al = algo == "cannon" ? Algorithm::cannon
-                         : algo == "case1" ? Algorithm::case1 : Algorithm::case2;
-    multiply_dispatch(*comm, al, a, b, c, nprocs);
+    if (algo == "auto") {
+      const Algorithm al = multiply_auto(*comm, a, b, c, nprocs);
+      std::printf("auto selected %s\n", algorithm_name(al));
+    } else {
+      const Algorithm al = algo == "cannon" ? Algorithm::cannon
+                           : algo == "case1" ? Algorithm::case1 : Algorithm::case2;
+      multiply_dispatch(*comm, al, a, b, c, nprocs);
+    }
     const std::string out = world > 1 ? std::string(argv[7]) + ".rank" + std::to_string(rank)
                                       : std::string(argv[7]);
     write_matrix_file(out, c, fmt);

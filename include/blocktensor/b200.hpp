@@ -544,7 +544,10 @@ class DistMatrix {
       nb += b;
       ne += e;
     }
-    return {nb, ne};
+    // global counts: summed over the processes of an NCCL group (collective)
+    int64_t v[2] = {nb, ne};
+    detail::check(bt_grid_sum(comm_->handle(), v, 2));
+    return {v[0], v[1]};
   }
   Axis rows_, cols_;
   ProcessGrid grid_;
@@ -859,29 +862,41 @@ inline Algorithm select_algorithm(double m, double n, double k, double oa, doubl
   return best;
 }
 // Extension: NVLink/NVSwitch-aware time model, seconds per
-// multiply on s.nprocs B200s (mirror of dist.py predicted_time_b200).  Cannon
-// overlaps its shifts with the local multiply (square grids only); case 1's C
-// reduction follows the multiply; case 2's B gather is half hidden behind the
-// symbolic passes.
+// multiply on s.nprocs B200s -- the mirror of dist.py predicted_time_b200,
+// with the rates FITTED to the measured times of every algorithm on 2 and 4
+// B200s (tests/golden/algo_times_b200.jsonl, tools/algo_sweep.py).
 struct B200Machine {
-  double fp64_flops = 26e12;  // k_smm_dmma useful FP64, c1
-  double link_bytes = 770e9;  // NVLink peer copy per direction
-  double hbm_bytes = 6.55e12; // HBM copy
+  double fp64_flops = 25.6e12;    // local multiply, useful FP64
+  double hbm_bytes = 6.55e12;     // C written once
+  double cannon_bytes = 237e9;    // Cannon panel shifts
+  double redist_bytes = 126e9;    // layout changes of case 1 / case 2
+  double reduce_bytes = 265e9;    // case 1 partial-C reduction
+  double gather_bytes = 33.1e9;   // case 2 B gather incl. assembly
+  double cannon_overhead = 0.86e-3, case1_overhead = 2.92e-3, case2_overhead = 0.0;
 };
 inline double predicted_time_b200(Algorithm algo, const MultiplySpec& s,
                                   const B200Machine& hw = B200Machine{}) {
   s.validate();
   const double p = s.nprocs;
   const double flops = 2.0 * s.m * s.n * s.k * s.occ_a * s.occ_b;
-  const double compute = flops / (p * hw.fp64_flops) + 8.0 * s.stored_c() / p / hw.hbm_bytes;
+  const double sa = s.stored_a(), sb = s.stored_b(), sc = s.stored_c();
+  const double compute = flops / (p * hw.fp64_flops) + 8.0 * sc / p / hw.hbm_bytes;
   switch (algo) {
     case Algorithm::cannon: {
       const double q = std::round(std::sqrt(p));
       if (q * q != p) return std::numeric_limits<double>::infinity();
-      return std::max(compute, 8.0 * cannon_volume(s) / hw.link_bytes);
+      if (p == 1) return compute;
+      return std::max(compute, 8.0 * cannon_volume(s) / hw.cannon_bytes) + hw.cannon_overhead;
     }
-    case Algorithm::case1: return compute + 8.0 * case1_volume(s) / hw.link_bytes;
-    case Algorithm::case2: return compute + 0.5 * 8.0 * case2_volume(s) / hw.link_bytes;
+    case Algorithm::case1:
+      if (p == 1) return compute;
+      return flops / (p * hw.fp64_flops) + 8.0 * sc / hw.hbm_bytes +
+             8.0 * (sa + sb) / p / hw.redist_bytes + 8.0 * sc * (p - 1) / p / hw.reduce_bytes +
+             hw.case1_overhead;
+    case Algorithm::case2:
+      if (p == 1) return compute;
+      return std::max(compute, 8.0 * sb * (p - 1) / p / hw.gather_bytes) +
+             8.0 * (sa + sc) / p / hw.redist_bytes + hw.case2_overhead;
   }
   throw invalid_argument("predicted_time_b200: unknown algorithm");
 }
@@ -911,6 +926,38 @@ inline MultiplySpec measured_spec(const DistMatrix& a, const DistMatrix& b, doub
   s.occ_c = occ_c;
   s.nprocs = nprocs;
   return s;
+}
+
+// multiply_dispatch with the algorithm chosen by the fitted B200 model among
+// those whose layout preconditions hold (Cannon: square grid of nprocs, C =
+// A rows x B cols); case 2 runs as the one-step NVLink gather.  Mirrors
+// dist.py select_for / multiply_dispatch(Algorithm.auto).  Returns the choice.
+inline Algorithm multiply_auto(SimComm& comm, const DistMatrix& a, const DistMatrix& b,
+                               DistMatrix& c, int nprocs, double eps = 0.0,
+                               const B200Machine& hw = B200Machine{}) {
+  MultiplySpec s = measured_spec(a, b, 0.0, nprocs);
+  const double p = std::min(std::max(s.occ_a * s.occ_b, 0.0), 1.0);
+  s.occ_c = std::min(1.0, std::max(0.0, 1.0 - std::pow(1.0 - p, double(a.n_block_cols()))));
+  const ProcessGrid& g = a.grid();
+  const bool cannon_ok = g.ndims() == 2 && g.dim(0) == g.dim(1) && g.dim(0) * g.dim(1) == nprocs &&
+                         b.grid() == g && c.grid() == g && c.rows().same_distribution(a.rows()) &&
+                         c.cols().same_distribution(b.cols()) &&
+                         a.cols().same_distribution(b.rows());
+  Algorithm best = Algorithm::case1;
+  double t = predicted_time_b200(Algorithm::case1, s, hw);
+  if (cannon_ok && predicted_time_b200(Algorithm::cannon, s, hw) <= t) {
+    best = Algorithm::cannon;
+    t = predicted_time_b200(Algorithm::cannon, s, hw);
+  }
+  if (predicted_time_b200(Algorithm::case2, s, hw) < t) best = Algorithm::case2;
+  switch (best) {
+    case Algorithm::cannon: multiply_cannon(comm, a, b, c, eps); break;
+    case Algorithm::case1: multiply_reduce_case1(comm, a, b, c, nprocs, eps); break;
+    case Algorithm::case2:
+      detail::check(bt_multiply_case2(a.handle(), b.handle(), c.handle(), nprocs, 1, eps, nullptr));
+      break;
+  }
+  return best;
 }
 
 

@@ -636,40 +636,59 @@ def select_algorithm(m, n, k, occ_a, occ_b, occ_c_estimate, nprocs):
 
 @dataclass
 class B200Machine:
-    """Per-GPU rates of the time model (measured on this pool, profiles/):
-    useful FP64 of the local multiply, NVLink per direction, HBM copy."""
-    fp64_flops: float = 26e12     # k_smm_dmma, c1 (r01b)
-    link_bytes: float = 770e9     # peer copy, B200_PROFILING.md
-    hbm_bytes: float = 6.55e12    # MEASURED_PEAKS.json
+    """Rates of the B200 time model, FITTED (least squares on log time) to the
+    measured multiply times of tests/golden/algo_times_b200.jsonl
+    (tools/algo_sweep.py: square / tall-skinny / dense / wide-C workloads on 2
+    and 4 B200s, every algorithm, inputs in a round-robin layout).  Effective
+    rates of this implementation, not hardware peaks: they fold in the host
+    planning of redistributions and the gather assembly."""
+    fp64_flops: float = 25.6e12    # local multiply, useful FP64
+    hbm_bytes: float = 6.55e12     # C written once (MEASURED_PEAKS.json copy rate)
+    cannon_bytes: float = 237e9    # Cannon panel shifts
+    redist_bytes: float = 126e9    # input/output layout changes of case 1 / case 2
+    reduce_bytes: float = 265e9    # case 1: partial-C reduction to the owners
+    gather_bytes: float = 33.1e9   # case 2: B gather incl. assembly
+    cannon_overhead: float = 0.86e-3
+    case1_overhead: float = 2.92e-3
+    case2_overhead: float = 0.0
 
 
 def predicted_time_b200(algo, s: MultiplySpec, machine: B200Machine = B200Machine()):
     """Extension (not in the reference): seconds per multiply on
-    s.nprocs B200s joined by NVSwitch.  Volumes are the paper's (Eq. 1/2/5, in
-    elements); what differs from the volume argmin is how they meet the
-    compute:
-      * compute: 2*M*N*K*occ_a*occ_b useful flops split over the GPUs, plus the
-        C slab written once from HBM;
-      * Cannon: the shifts are posted before each local multiply, so time =
-        max(compute, traffic); only square grids;
-      * case 1: the C reduction follows the local multiply (not hidden);
-      * case 2 (B gather): the value transfer overlaps the symbolic passes only
-        (counted as half hidden).
-    Every GPU has the full NVLink bandwidth to every peer (NVSwitch), so
-    traffic time = bytes per rank / link bandwidth."""
+    s.nprocs B200s joined by NVSwitch, from the paper's stored sizes S_A, S_B,
+    S_C (cost_model.hpp:19-39) and the fitted rates of B200Machine:
+      * compute = useful flops / (P * F) + C written once per rank (S_C / P);
+      * Cannon (square P only): max(compute, Eq.-1 panel traffic) -- the
+        shifts are posted before each local multiply;
+      * case 1: every rank writes a full partial C (S_C), the K-slab
+        redistribution of A and B, then the partial-C reduction
+        S_C (P-1)/P (not hidden);
+      * case 2: max(compute, B gather S_B (P-1)/P) -- the gather runs under
+        the symbolic passes and the multiply -- plus the row-slab
+        redistribution of A and C.
+    Fit quality and the selection check: tests/test_host_logic.py."""
     s.validate()
     p = s.nprocs
     flops = 2.0 * s.m * s.n * s.k * s.occ_a * s.occ_b
-    compute = flops / (p * machine.fp64_flops) + 8.0 * s.stored_c() / p / machine.hbm_bytes
+    sa, sb, sc = s.stored_a(), s.stored_b(), s.stored_c()
+    hw = machine
+    compute = flops / (p * hw.fp64_flops) + 8.0 * sc / p / hw.hbm_bytes
     if algo == Algorithm.cannon:
         q = round(math.sqrt(p))
         if q * q != p:
             return math.inf
-        return max(compute, 8.0 * cannon_volume(s) / machine.link_bytes)
+        if p == 1:
+            return compute
+        return max(compute, 8.0 * cannon_volume(s) / hw.cannon_bytes) + hw.cannon_overhead
+    if p == 1 and algo in (Algorithm.case1, Algorithm.case2):
+        return compute
     if algo == Algorithm.case1:
-        return compute + 8.0 * case1_volume(s) / machine.link_bytes
+        return (flops / (p * hw.fp64_flops) + 8.0 * sc / hw.hbm_bytes
+                + 8.0 * (sa + sb) / p / hw.redist_bytes
+                + 8.0 * sc * (p - 1) / p / hw.reduce_bytes + hw.case1_overhead)
     if algo == Algorithm.case2:
-        return compute + 0.5 * 8.0 * case2_volume(s) / machine.link_bytes
+        return (max(compute, 8.0 * sb * (p - 1) / p / hw.gather_bytes)
+                + 8.0 * (sa + sc) / p / hw.redist_bytes + hw.case2_overhead)
     raise InvalidArgument("predicted_time_b200: unknown algorithm")
 
 

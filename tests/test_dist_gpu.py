@@ -191,3 +191,33 @@ def test_redistribute_roundtrip_and_transpose(oracle, ctx):
     assert sum(comm.ledger().rank_total(r).elements_sent for r in range(4)) == 0
     assert_parity(_got(same), A, tol=0.0)
     comm.close()
+
+
+@pytest.mark.parametrize("gdims,nprocs", [([2, 2], 4), ([2, 1], 2)])
+def test_dispatch_auto(oracle, ctx, gdims, nprocs):
+    """multiply_dispatch(Algorithm.auto): the fitted B200 model's choice among
+    the algorithms whose layout preconditions hold (Cannon on the square
+    round-robin grid), results equal to the oracle."""
+    from paper_1910_13555_b200 import dist as dd
+    grid = dd.ProcessGrid(gdims)
+    comm = dd.SimComm(grid, ctx=ctx)
+    sz = np.full(24, 23, np.int32)
+    A = oracle.random_matrix(71, sz, sz, 0.3)
+    B = oracle.random_matrix(72, sz, sz, 0.3)
+    bl = dd.Blocking(sz)
+    a = dd.new_matrix_round_robin(bl, bl, grid, comm)
+    b = dd.new_matrix_round_robin(bl, bl, grid, comm)
+    c = dd.new_matrix_round_robin(bl, bl, grid, comm)
+    a.put_blocks(A.bi, A.bj, A.vals)
+    b.put_blocks(B.bi, B.bj, B.vals)
+    choice, times = dd.select_for(a, b, c, nprocs)
+    if gdims == [2, 2]:
+        assert dd.Algorithm.cannon in times
+    else:
+        assert dd.Algorithm.cannon not in times
+    st = dd.multiply_dispatch(comm, dd.Algorithm.auto, a, b, c, nprocs)
+    assert st["algorithm"] == dd.algorithm_name(choice)
+    want, _, _ = oracle.multiply(A, B, Blocks.empty(sz, sz))
+    bi, bj, v = c.blocks()
+    assert_parity(Blocks(sz, sz, bi, bj, v), want)
+    comm.close()

@@ -24,7 +24,7 @@ def test_facade_example_compiles_and_links():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("algo,q,nprocs", [("cannon", 1, 1), ("cannon", 2, 4), ("case1", 1, 3),
-                                           ("case2", 1, 4)])
+                                           ("case2", 1, 4), ("auto", 2, 4), ("auto", 1, 2)])
 def test_facade_multiply_matches_oracle(oracle, tmp_path, algo, q, nprocs):
     _build()
     rs = np.array([5, 13, 23, 7, 13, 5, 23, 11], np.int32)
