@@ -261,6 +261,11 @@ class SimComm {
     detail::check(bt_grid_create(ctx_, grid_.size(), &g_));
     current() = this;
   }
+  // a group over an existing context (a subgroup from bt_ctx_split); owns it
+  SimComm(ProcessGrid grid, bt_ctx* ctx) : grid_(std::move(grid)), ctx_(ctx) {
+    detail::check(bt_grid_create(ctx_, grid_.size(), &g_));
+    current() = this;
+  }
   // this process's ranks: all of them (virtual ranks) or its own (NCCL)
   std::vector<int> local_ranks() const {
     int n = 0, first = 0, nl = 0;
@@ -960,6 +965,235 @@ inline Algorithm multiply_auto(SimComm& comm, const DistMatrix& a, const DistMat
   return best;
 }
 
+
+// ------------------------------------------------------------- tall-skinny
+// SPEC.md:415-477 (the reference has this module only in its spec): a
+// tall-and-skinny matrix split along its long dimension into f approximately
+// square submatrices, index data along that dimension supplied by functions
+// (IndexFuncs, the spec's form of Axis::functional) so no host array spans the
+// full split dimension.  Submatrix s lives on SUBGROUP s of the ranks:
+//  * one rank per process (NCCL): ranks [s*P/f, (s+1)*P/f) with their own
+//    communicator (bt_ctx_split); this process holds its subgroup's submatrix
+//    only, and the subgroups multiply concurrently;
+//  * virtual ranks (one process): one SimComm per subgroup on this GPU, the
+//    subgroups run one after another (the spec's sequential schedule).
+// multiply_tall_skinny supports the K split (A split on columns, B on rows,
+// C a plain DistMatrix of the parent group): C += sum_s A_s B_s, the partial
+// C of every subgroup reduced into C with redistribute_add on the parent
+// group (ledger phase "ts_reduce", the spec's cross-subgroup reduction).
+struct IndexFuncs {
+  std::int64_t n_blocks = 0;
+  std::function<int(std::int64_t)> block_size_fn;
+  std::function<int(std::int64_t)> dist_fn;
+  int size(std::int64_t b) const {
+    if (b < 0 || b >= n_blocks) throw invalid_argument("IndexFuncs: block out of range");
+    const int v = block_size_fn(b);
+    if (v < 1) throw invalid_argument("IndexFuncs: block sizes must be >= 1");
+    return v;
+  }
+  int dist(std::int64_t b) const { return dist_fn(b); }
+};
+
+// ceiling partition: the first submatrices get ceil(n/f) block indices
+inline std::vector<std::pair<std::int64_t, std::int64_t>> ceil_partition(std::int64_t n, int f) {
+  if (f < 1) throw invalid_argument("ceil_partition: factor must be >= 1");
+  const std::int64_t w = n ? (n + f - 1) / f : 0;
+  std::vector<std::pair<std::int64_t, std::int64_t>> out;
+  for (int s = 0; s < f; ++s) out.emplace_back(std::min(n, s * w), std::min(n, (s + 1) * w));
+  return out;
+}
+
+// argmin over f in 1..P of |long/f - short| in element units, ties to smaller f
+inline int choose_split_factor(double long_elems, double short_elems, int nprocs) {
+  if (long_elems <= 0 || short_elems <= 0 || nprocs < 1)
+    throw invalid_argument("choose_split_factor: inputs must be positive");
+  int best = 1;
+  double bd = std::fabs(long_elems - short_elems);
+  for (int f = 2; f <= nprocs; ++f) {
+    const double d = std::fabs(long_elems / f - short_elems);
+    if (d < bd) {
+      best = f;
+      bd = d;
+    }
+  }
+  return best;
+}
+
+// The f subgroups of a parent group (shared by every tall-skinny matrix of
+// one contraction): P/f ranks each, contiguous, on a sub_grid of that size.
+class Subgroups {
+ public:
+  Subgroups(SimComm& parent, int factor, ProcessGrid sub_grid)
+      : parent_(&parent), f_(factor), sub_grid_(std::move(sub_grid)) {
+    const int P = parent.nranks();
+    if (factor < 1 || P % factor != 0 || sub_grid_.size() != P / factor)
+      throw invalid_argument("Subgroups: factor must divide the group and sub_grid hold P/f ranks");
+    const std::vector<int> mine = parent.local_ranks();
+    if (static_cast<int>(mine.size()) == P) {  // virtual ranks: one SimComm per subgroup
+      for (int s = 0; s < f_; ++s) {
+        local_.push_back(s);
+        comms_.emplace_back(new SimComm(sub_grid_));
+      }
+    } else {                                    // NCCL: this process's subgroup
+      const int r = mine.at(0), s = r / (P / f_);
+      bt_ctx* sub = nullptr;
+      detail::check(bt_ctx_split(parent.context(), s, r, &sub));
+      local_.push_back(s);
+      comms_.emplace_back(new SimComm(sub_grid_, sub));
+    }
+    SimComm::current() = &parent;
+  }
+  int factor() const noexcept { return f_; }
+  const ProcessGrid& sub_grid() const noexcept { return sub_grid_; }
+  SimComm& parent() const noexcept { return *parent_; }
+  // subgroups held by this process and their communicators
+  const std::vector<int>& local() const noexcept { return local_; }
+  SimComm& comm_of(int s) const {
+    for (std::size_t t = 0; t < local_.size(); ++t)
+      if (local_[t] == s) return *comms_[t];
+    throw ownership_error("Subgroups: subgroup " + std::to_string(s) + " lives in another process");
+  }
+  int first_parent_rank(int s) const { return s * sub_grid_.size(); }
+
+ private:
+  SimComm* parent_;
+  int f_;
+  ProcessGrid sub_grid_;
+  std::vector<int> local_;
+  std::vector<std::unique_ptr<SimComm>> comms_;
+};
+
+enum class SplitDim { rows, cols };
+
+class TallSkinnyMatrix {
+ public:
+  TallSkinnyMatrix(Subgroups& groups, IndexFuncs rows, IndexFuncs cols, SplitDim dim)
+      : groups_(&groups), rows_(std::move(rows)), cols_(std::move(cols)), dim_(dim) {
+    const std::int64_t n = dim == SplitDim::rows ? rows_.n_blocks : cols_.n_blocks;
+    ranges_ = ceil_partition(n, groups.factor());
+    const ProcessGrid& g = groups.sub_grid();
+    for (int s : groups.local()) {
+      const auto r = ranges_[static_cast<std::size_t>(s)];
+      // functional axes over the submatrix's range only (no full-length arrays)
+      auto axis = [&](const IndexFuncs& f, std::int64_t b0, std::int64_t nb, int extent) {
+        const IndexFuncs fc = f;
+        return Axis::functional(
+            nb, [fc, b0](std::int64_t b) { return fc.size(b0 + b); },
+            [fc, b0, extent](std::int64_t b) { return ((fc.dist(b0 + b) % extent) + extent) % extent; },
+            extent);
+      };
+      Axis ra = dim == SplitDim::rows ? axis(rows_, r.first, r.second - r.first, g.dim(0))
+                                      : axis(rows_, 0, rows_.n_blocks, g.dim(0));
+      Axis ca = dim == SplitDim::cols ? axis(cols_, r.first, r.second - r.first, g.dim(1))
+                                      : axis(cols_, 0, cols_.n_blocks, g.dim(1));
+      subs_.emplace_back(s, std::unique_ptr<DistMatrix>(
+                                new DistMatrix(std::move(ra), std::move(ca), g, &groups.comm_of(s))));
+      index_len_.push_back(r.second - r.first);
+    }
+  }
+  SplitDim split_dim() const noexcept { return dim_; }
+  int factor() const noexcept { return groups_->factor(); }
+  const IndexFuncs& rows() const noexcept { return rows_; }
+  const IndexFuncs& cols() const noexcept { return cols_; }
+  Subgroups& groups() const noexcept { return *groups_; }
+  const std::vector<std::pair<std::int64_t, std::int64_t>>& ranges() const noexcept { return ranges_; }
+  // global split-dimension block -> (submatrix, local index), and back
+  std::pair<int, std::int64_t> locate(std::int64_t b) const {
+    const std::int64_t n = ranges_.empty() ? 0 : ranges_.back().second;
+    if (b < 0 || b >= n) throw invalid_argument("TallSkinnyMatrix: block out of range");
+    const std::int64_t w = ranges_[0].second - ranges_[0].first;
+    const int s = static_cast<int>(b / w);
+    return {s, b - ranges_[static_cast<std::size_t>(s)].first};
+  }
+  std::int64_t global_index(int s, std::int64_t local) const {
+    const auto r = ranges_.at(static_cast<std::size_t>(s));
+    if (local < 0 || local >= r.second - r.first) throw invalid_argument("TallSkinnyMatrix: local index out of range");
+    return r.first + local;
+  }
+  bool holds(int s) const {
+    for (const auto& p : subs_)
+      if (p.first == s) return true;
+    return false;
+  }
+  DistMatrix& sub(int s) const {
+    for (const auto& p : subs_)
+      if (p.first == s) return *p.second;
+    throw ownership_error("TallSkinnyMatrix: submatrix " + std::to_string(s) + " lives in another process");
+  }
+  // put_block routed to its submatrix; blocks of another process's subgroup
+  // are skipped (each process puts its own share) -- returns whether stored
+  bool put_block(std::int64_t i, std::int64_t j, DenseBlock block, bool accumulate = false) {
+    const auto loc = locate(dim_ == SplitDim::rows ? i : j);
+    if (!holds(loc.first)) return false;
+    DistMatrix& m = sub(loc.first);
+    const std::int64_t li = dim_ == SplitDim::rows ? loc.second : i;
+    const std::int64_t lj = dim_ == SplitDim::rows ? j : loc.second;
+    if (!m.comm()->is_local(m.owner_rank(li, lj))) return false;
+    m.put_block(li, lj, std::move(block), accumulate);
+    return true;
+  }
+  // host index entries along the split dimension resident in this process
+  // (functional axes: none) and the longest device index range (one submatrix)
+  std::int64_t host_index_entries() const {
+    std::int64_t e = 0;
+    for (const auto& p : subs_) e += p.second->rows().index_entries() + p.second->cols().index_entries();
+    return e;
+  }
+  std::int64_t max_device_index_range() const {
+    std::int64_t m = 0;
+    for (auto v : index_len_) m = std::max(m, v);
+    return m;
+  }
+
+ private:
+  Subgroups* groups_;
+  IndexFuncs rows_, cols_;
+  SplitDim dim_;
+  std::vector<std::pair<std::int64_t, std::int64_t>> ranges_;
+  std::vector<std::pair<int, std::unique_ptr<DistMatrix>>> subs_;
+  std::vector<std::int64_t> index_len_;
+};
+
+// C += A * B with A split on K (columns) and B on K (rows) over the same
+// subgroups; C is a DistMatrix of the parent group.  Each subgroup multiplies
+// its pair (multiply_auto picks the algorithm on the subgroup), then the
+// partial C blocks are reduced into C across subgroups (redistribute_add on
+// the parent group, ledger phase "ts_reduce").
+inline void multiply_tall_skinny(const TallSkinnyMatrix& a, const TallSkinnyMatrix& b,
+                                 DistMatrix& c, double eps = 0.0) {
+  if (a.split_dim() != SplitDim::cols || b.split_dim() != SplitDim::rows)
+    throw layout_error("k", "multiply_tall_skinny: the C++ layer runs the K split (A split on "
+                            "columns, B on rows); M/N splits: paper_1910_13555_b200/tall_skinny.py");
+  if (&a.groups() != &b.groups())
+    throw layout_error("k", "multiply_tall_skinny: A and B must share their subgroups");
+  if (a.cols().n_blocks != b.rows().n_blocks)
+    throw layout_error("k", "multiply_tall_skinny: contracted dimension splits differ");
+  for (std::int64_t t = 0; t < a.cols().n_blocks; ++t)
+    if (a.cols().size(t) != b.rows().size(t))
+      throw layout_error("k", "multiply_tall_skinny: contracted dimension blockings differ");
+  Subgroups& g = a.groups();
+  SimComm& parent = g.parent();
+  // partial C of every local subgroup, then staged into a parent-group matrix
+  DistMatrix partial(Axis::round_robin(c.rows().blocking(), c.grid().dim(0)),
+                     Axis::round_robin(c.cols().blocking(), c.grid().dim(1)), c.grid(), &parent);
+  for (int s : g.local()) {
+    SimComm& sc = g.comm_of(s);
+    const ProcessGrid& sg = g.sub_grid();
+    DistMatrix cs(Axis::round_robin(c.rows().blocking(), sg.dim(0)),
+                  Axis::round_robin(c.cols().blocking(), sg.dim(1)), sg, &sc);
+    multiply_auto(sc, a.sub(s), b.sub(s), cs, sg.size(), eps);
+    for (int r = 0; r < sg.size(); ++r) {
+      if (!sc.is_local(r)) continue;
+      bt_mat* src = cs.local(r).handle();
+      const int pr = g.first_parent_rank(s) + r;
+      if (!parent.is_local(pr)) continue;
+      bt_mat* dst = partial.local(pr).handle();
+      detail::check(bt_mat_copy(src, dst));
+    }
+  }
+  redistribute_add(parent, partial, c, "ts_reduce");
+  SimComm::current() = &parent;
+}
 
 // ------------------------------------------------------------------ tensors
 // SPEC.md:479-545 (the tensor module exists only in the reference's spec):

@@ -73,6 +73,11 @@ int bt_version(void);
  * unique id (bt_get_unique_id on rank 0, broadcast by the caller) and its rank. */
 int bt_get_unique_id(void* id128);
 int bt_ctx_create(int device, int nranks, int rank, const void* nccl_id, bt_ctx** out);
+/* A subgroup context (SPEC.md tall_skinny subgroups): every process of the
+ * parent's NCCL group calls it; processes with the same color form one
+ * subgroup (ranks ordered by key) with its own communicator -- ncclCommSplit.
+ * A one-rank subgroup is a single-GPU context.  The parent must have nranks > 1. */
+int bt_ctx_split(bt_ctx* parent, int color, int key, bt_ctx** out);
 int bt_ctx_destroy(bt_ctx* ctx);
 /* waits for all device work of the context (incl. asynchronous exports) */
 int bt_ctx_sync(bt_ctx* ctx);

@@ -73,6 +73,7 @@ SIGNATURES = {
     "bt_get_unique_id": (C.c_int, [C.c_void_p]),
     "bt_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     "bt_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "bt_ctx_split": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "bt_ctx_sync": (C.c_int, [C.c_void_p]),
     "bt_ctx_rank": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "bt_ctx_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),

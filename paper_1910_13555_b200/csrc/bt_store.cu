@@ -440,6 +440,39 @@ int bt_get_unique_id(void* id128) {
   });
 }
 
+// device, streams, pool, pinned staging and events of a new context
+static bt_ctx* new_ctx(int device) {
+  int ndev = 0;
+  BT_CUDA(cudaGetDeviceCount(&ndev));
+  BT_REQUIRE(device >= 0 && device < ndev, BT_ERR_INVALID_ARGUMENT,
+             "bt_ctx_create: device " + std::to_string(device) + " not present (" +
+                 std::to_string(ndev) + " visible)");
+  BT_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  BT_CUDA(cudaGetDeviceProperties(&prop, device));
+  BT_REQUIRE(prop.major == 10, BT_ERR_CUDA,
+             std::string("libbtcuda is built for sm_100a (B200); device is ") + prop.name);
+  auto* c = new bt_ctx;
+  Ctx& x = c->impl;
+  x.device = device;
+  x.num_sms = prop.multiProcessorCount;
+  x.smem_optin = prop.sharedMemPerBlockOptin;
+  BT_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
+  cudaMemPool_t pool;
+  BT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  BT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  BT_CUDA(cudaHostAlloc(&x.pinned, 4096, cudaHostAllocMapped));
+  BT_CUDA(cudaHostGetDevicePointer(&x.pinned_dev, x.pinned, 0));
+  BT_CUDA(cudaEventCreateWithFlags(&x.stage_ev, cudaEventDisableTiming));
+  for (auto& e : x.ev) BT_CUDA(cudaEventCreate(&e));
+  for (auto& a : x.aux) BT_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+  BT_CUDA(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming));
+  for (auto& e : x.xfer_done) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : x.ev_join) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return c;
+}
+
 int bt_ctx_create(int device, int nranks, int rank, const void* nccl_id, bt_ctx** out) {
   return guard([&] {
     BT_REQUIRE(out, BT_ERR_INVALID_ARGUMENT, "null output handle");
@@ -447,47 +480,46 @@ int bt_ctx_create(int device, int nranks, int rank, const void* nccl_id, bt_ctx*
                "bt_ctx_create: bad rank/nranks");
     BT_REQUIRE(nranks == 1 || nccl_id, BT_ERR_INVALID_ARGUMENT,
                "bt_ctx_create: nranks > 1 needs an NCCL unique id");
-    int ndev = 0;
-    BT_CUDA(cudaGetDeviceCount(&ndev));
-    BT_REQUIRE(device >= 0 && device < ndev, BT_ERR_INVALID_ARGUMENT,
-               "bt_ctx_create: device " + std::to_string(device) + " not present (" +
-                   std::to_string(ndev) + " visible)");
-    BT_CUDA(cudaSetDevice(device));
-    cudaDeviceProp prop;
-    BT_CUDA(cudaGetDeviceProperties(&prop, device));
-    BT_REQUIRE(prop.major == 10, BT_ERR_CUDA,
-               std::string("libbtcuda is built for sm_100a (B200); device is ") + prop.name);
-    auto* c = new bt_ctx;
+    bt_ctx* c = new_ctx(device);
     Ctx& x = c->impl;
-    x.device = device;
     x.nranks = nranks;
     x.rank = rank;
-    x.num_sms = prop.multiProcessorCount;
-    x.smem_optin = prop.sharedMemPerBlockOptin;
-    BT_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
-    cudaMemPool_t pool;
-    BT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-    uint64_t thr = UINT64_MAX;
-    BT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    BT_CUDA(cudaHostAlloc(&x.pinned, 4096, cudaHostAllocMapped));
-    BT_CUDA(cudaHostGetDevicePointer(&x.pinned_dev, x.pinned, 0));
-    BT_CUDA(cudaEventCreateWithFlags(&x.stage_ev, cudaEventDisableTiming));
-    for (auto& e : x.ev) BT_CUDA(cudaEventCreate(&e));
-    for (auto& a : x.aux) BT_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
-    BT_CUDA(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming));
-    for (auto& e : x.xfer_done) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& e : x.ev_join) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     if (nranks > 1) {
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, 128);
       ncclComm_t comm;
       ncclResult_t r = ncclCommInitRank(&comm, nranks, id, rank);
       if (r != ncclSuccess) {
-        cudaStreamDestroy(x.stream);
-        delete c;
+        bt_ctx_destroy(c);
         throw Error(BT_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
       }
       x.nccl = comm;
+    }
+    *out = c;
+  });
+}
+
+int bt_ctx_split(bt_ctx* parent, int color, int key, bt_ctx** out) {
+  return guard([&] {
+    BT_REQUIRE(parent && out, BT_ERR_INVALID_ARGUMENT, "null argument");
+    BT_REQUIRE(parent->impl.nccl, BT_ERR_INVALID_ARGUMENT,
+               "bt_ctx_split: the parent context has no NCCL communicator (one process holds "
+               "every rank: use one context per subgroup instead)");
+    BT_REQUIRE(color >= 0, BT_ERR_INVALID_ARGUMENT, "bt_ctx_split: color must be >= 0");
+    ncclComm_t sub = nullptr;
+    ncclResult_t r = ncclCommSplit(static_cast<ncclComm_t>(parent->impl.nccl), color, key, &sub,
+                                   nullptr);
+    BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(r));
+    int n = 1, me = 0;
+    ncclCommCount(sub, &n);
+    ncclCommUserRank(sub, &me);
+    bt_ctx* c = new_ctx(parent->impl.device);
+    c->impl.nranks = n;
+    c->impl.rank = me;
+    if (n > 1) {
+      c->impl.nccl = sub;
+    } else {
+      ncclCommDestroy(sub);  // a one-rank subgroup is a plain single-GPU context
     }
     *out = c;
   });

@@ -160,3 +160,75 @@ def test_facade_multiply_files_nccl(oracle, tmp_path, world, algo, q, nprocs):
     got = Blocks(rs, ns, bi[order], bj[order], np.concatenate([blocks[t] for t in order]))
     want, _, _ = oracle.multiply(A, B, Cin)
     assert_parity(got, want)
+
+
+def _ts_case(oracle, tmp_path):
+    rs = np.array([4, 3, 5, 4, 2, 4, 3, 5], np.int32)        # M: 8 blocks
+    ks = np.array([3, 4, 5, 2] * 32, np.int32)               # K: 128 blocks (the long dim)
+    ns = np.array([5, 4, 3, 4, 4, 2, 5, 3], np.int32)        # N: 8 blocks
+    A = oracle.random_matrix(81, rs, ks, 0.5)
+    B = oracle.random_matrix(82, ks, ns, 0.5)
+    pa, pb, pc = (str(tmp_path / n) for n in ("a.bin", "b.bin", "c.bin"))
+    write_matrix_binary(pa, A)
+    write_matrix_binary(pb, B)
+    from oracle.oracle import Blocks
+    want, _, _ = oracle.multiply(A, B, Blocks.empty(rs, ns))
+    return (rs, ns), pa, pb, pc, want
+
+
+def _merge_parts(paths, rs, ns):
+    from oracle.oracle import Blocks
+    parts = [read_matrix_binary(p) for p in paths]
+    bi = np.concatenate([p.bi for p in parts])
+    bj = np.concatenate([p.bj for p in parts])
+    blocks = []
+    for p in parts:
+        off = p.offsets()
+        blocks += [p.vals[off[t]:off[t + 1]] for t in range(p.nblk)]
+    order = np.lexsort((bj, bi))
+    vals = np.concatenate([blocks[t] for t in order]) if len(order) else np.zeros(0)
+    return Blocks(rs, ns, bi[order], bj[order], vals)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("f,sr,sc", [(1, 2, 2), (2, 2, 1), (4, 1, 1)])
+def test_facade_tall_skinny_virtual_subgroups(oracle, tmp_path, f, sr, sc):
+    """C++ tall-skinny layer, K split into f subgroups of
+    virtual ranks (SPEC example: A 8x128 blocks split f=4 on K, B 128x8):
+    C equals the oracle; the cross-subgroup reduction is charged to the
+    ledger (f > 1); a 10^4-block split dimension keeps no host index array and
+    device index ranges of one submatrix (ceil(10^4/f))."""
+    _build()
+    (rs, ns), pa, pb, pc, want = _ts_case(oracle, tmp_path)
+    r = subprocess.run([os.path.join(ROOT, "examples", "tall_skinny"), str(f), str(sr), str(sc),
+                        pa, pb, pc], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert_parity(_merge_parts([pc], rs, ns), want)
+    import re
+    m = re.search(r"ts_reduce elements sent (\d+), host index entries (\d+), max device index "
+                  r"range (\d+)", r.stdout)
+    assert m, r.stdout
+    assert (int(m.group(1)) > 0) == (f > 1)
+    assert int(m.group(2)) == 0 and int(m.group(3)) == -(-10000 // f)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("f,sr,sc", [(2, 2, 1), (4, 1, 1)])
+def test_facade_tall_skinny_nccl_subgroups(oracle, tmp_path, f, sr, sc):
+    """The same with one rank per GPU: subgroups are NCCL communicators split
+    from the parent (bt_ctx_split) and multiply concurrently."""
+    import sys
+    import torch
+    world = f * sr * sc
+    if not torch.cuda.is_available() or torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    _build()
+    (rs, ns), pa, pb, pc, want = _ts_case(oracle, tmp_path)
+    env = dict(os.environ, BT_NCCL_ID_FILE=str(tmp_path / "nccl_id"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29750 + f), "--no-python", os.path.join(ROOT, "examples", "tall_skinny"),
+           str(f), str(sr), str(sc), pa, pb, pc]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert_parity(_merge_parts([pc + f".rank{k}" for k in range(world)], rs, ns), want)
