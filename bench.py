@@ -39,9 +39,9 @@ NB, BS, OCC = 400, 23, 0.10
 SEED_A, SEED_B = 1001, 1002
 FP64_PEAK_TFLOPS = 37.1   # measured: tools/microbench/fp64_peak.cu on B200 (profiles/)
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_smm_dmma launch on this
-# workload, from `ncu --set full` of this bench (profiles/r01_final/ncu_dmma_bench_raw.csv):
-# 0.620 GB read + 0.695 GB written (algorithmic: 0.80 GB)
-NCU_TRAFFIC_BYTES = 1.316e9
+# workload, from `ncu --set full` of this bench (profiles/r02/ncu_bench_dmma_summary.txt):
+# 0.588 GB read + 0.694 GB written (algorithmic: 0.80 GB)
+NCU_TRAFFIC_BYTES = 1.2825e9
 
 
 METRIC = "block-sparse FP64 useful GFLOP/s"
