@@ -86,9 +86,14 @@ int bt_ctx_rank(const bt_ctx* ctx, int* rank, int* nranks);
 int bt_ctx_stream(bt_ctx* ctx, void** stream);
 /* number of kernels this context has launched so far */
 int bt_ctx_kernel_count(const bt_ctx* ctx, int64_t* count);
-/* on != 0: multiplies record CUDA events around their kernels and report
- * device times in bt_stats (adds one stream sync per call) */
+/* 0: off.  1: multiplies record CUDA events around their kernels and report
+ * device times in bt_stats (the call waits for its kernels).  2: events only;
+ * bt_multiply returns without waiting and bt_ctx_last_timing reads the times
+ * of the last multiply (waiting for it).  bt_multiply never waits for its
+ * numeric phase otherwise: results are stream-ordered, every later call on
+ * the context (export, get_block, ...) sees the finished C. */
 int bt_ctx_set_timing(bt_ctx* ctx, int on);
+int bt_ctx_last_timing(bt_ctx* ctx, double* ms_numeric, double* ms_total);
 
 /* ----------------------------------------------------------------- matrix */
 /* new_matrix (matrix.hpp:404-418) for one rank's store: blockings only; the

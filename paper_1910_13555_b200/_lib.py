@@ -79,6 +79,7 @@ SIGNATURES = {
     "bt_ctx_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "bt_ctx_kernel_count": (C.c_int, [C.c_void_p, _i64p]),
     "bt_ctx_set_timing": (C.c_int, [C.c_void_p, C.c_int]),
+    "bt_ctx_last_timing": (C.c_int, [C.c_void_p, _f64p, _f64p]),
     "bt_mat_create": (C.c_int, [C.c_void_p, C.c_int64, _i32p, C.c_int64, _i32p,
                                 C.POINTER(C.c_void_p)]),
     "bt_mat_destroy": (C.c_int, [C.c_void_p]),

@@ -136,7 +136,11 @@ struct Ctx {
   size_t hstage_cap = 0;
   cudaEvent_t stage_ev = nullptr;
   unsigned char* host_stage(size_t bytes);
-  bool timing = false;          // record CUDA events around multiply kernels
+  // 0: off; 1: CUDA events around the multiply kernels, the call waits for
+  // them and fills bt_stats; 2: events only, read later with
+  // bt_ctx_last_timing (the call does not wait)
+  int timing = 0;
+  bool last_had_numeric = false;  // the last multiply launched a numeric phase
   static constexpr int kAux = 16;  // side streams: concurrent per-class numeric kernels
   cudaStream_t aux[kAux] = {};
   cudaEvent_t ev_fork = nullptr;
@@ -266,9 +270,12 @@ void upload_parts(Ctx& x, const HostPart* parts, int n, void* const* dst);
 // implemented in bt_multiply.cu: C += A*B on one rank's stores (throws bt::Error)
 // wait_numeric (optional): the numeric phase waits for this event (B's values
 // may still be in flight while the symbolic passes run).
+// sync_at_end: wait for the numeric phase before returning (the distributed
+// drivers rely on it); the single-GPU C-ABI call returns right after enqueuing
+// (stream-ordered: every later call on the context sees the finished C).
 void local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& C, double eps, bt_stats* stats,
                     cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr,
-                    const std::function<void()>* after_sizes = nullptr);
+                    const std::function<void()>* after_sizes = nullptr, bool sync_at_end = true);
 
 }  // namespace bt
 

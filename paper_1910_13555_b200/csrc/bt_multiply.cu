@@ -950,7 +950,7 @@ using namespace bt;
 // The local multiply C += A*B (one rank's stores); throws bt::Error.
 void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps, bt_stats* stats,
                         cudaEvent_t wait_numeric, cudaEvent_t numeric_start,
-                        const std::function<void()>* after_sizes) {
+                        const std::function<void()>* after_sizes, bool sync_at_end) {
   {
     BT_REQUIRE(A.ctx == &x && B.ctx == &x && Cm.ctx == &x, BT_ERR_INVALID_ARGUMENT,
                "bt_multiply: matrices belong to another context");
@@ -1375,9 +1375,10 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     Cm.nelems = nelems;
     if (x.timing) BT_CUDA(cudaEventRecord(x.ev[3], st));
     tr.mark("numeric enqueued");
-    BT_CUDA(cudaStreamSynchronize(st));
+    x.last_had_numeric = nout > 0;
+    if (sync_at_end || x.timing == 1) BT_CUDA(cudaStreamSynchronize(st));
     tr.mark("final sync");
-    if (x.timing) {
+    if (x.timing == 1) {
       float ms = 0;
       if (nout > 0) {
         BT_CUDA(cudaEventElapsedTime(&ms, x.ev[1], x.ev[2]));
@@ -1406,6 +1407,29 @@ extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_m
                            double eps, bt_stats* stats) {
   return guard([&] {
     BT_REQUIRE(ctx && ah && bh && ch, BT_ERR_INVALID_ARGUMENT, "null argument");
-    local_multiply(ctx->impl, ah->impl, bh->impl, ch->impl, eps, stats);
+    local_multiply(ctx->impl, ah->impl, bh->impl, ch->impl, eps, stats, nullptr, nullptr, nullptr,
+                   false);
+  });
+}
+
+extern "C" int bt_ctx_last_timing(bt_ctx* ctx, double* ms_numeric, double* ms_total) {
+  return guard([&] {
+    BT_REQUIRE(ctx, BT_ERR_INVALID_ARGUMENT, "null context");
+    Ctx& x = ctx->impl;
+    BT_REQUIRE(x.timing != 0, BT_ERR_INVALID_ARGUMENT,
+               "bt_ctx_last_timing: timing is off (bt_ctx_set_timing)");
+    BT_CUDA(cudaEventSynchronize(x.ev[3]));
+    float ms = 0;
+    if (ms_numeric) {
+      *ms_numeric = 0;
+      if (x.last_had_numeric) {
+        BT_CUDA(cudaEventElapsedTime(&ms, x.ev[1], x.ev[2]));
+        *ms_numeric = ms;
+      }
+    }
+    if (ms_total) {
+      BT_CUDA(cudaEventElapsedTime(&ms, x.ev[0], x.ev[3]));
+      *ms_total = ms;
+    }
   });
 }

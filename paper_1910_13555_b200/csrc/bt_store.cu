@@ -587,7 +587,8 @@ int bt_ctx_kernel_count(const bt_ctx* c, int64_t* count) {
 int bt_ctx_set_timing(bt_ctx* c, int on) {
   return guard([&] {
     BT_REQUIRE(c, BT_ERR_INVALID_ARGUMENT, "null context");
-    c->impl.timing = on != 0;
+    BT_REQUIRE(on >= 0 && on <= 2, BT_ERR_INVALID_ARGUMENT, "bt_ctx_set_timing: mode 0, 1 or 2");
+    c->impl.timing = on;
   });
 }
 

@@ -63,8 +63,16 @@ class Context:
         check(self.lib.bt_ctx_stream(self.h, C.byref(s)), "bt_ctx_stream")
         return s.value or 0
 
-    def set_timing(self, on: bool = True):
-        check(self.lib.bt_ctx_set_timing(self.h, int(bool(on))), "bt_ctx_set_timing")
+    def set_timing(self, on=True):
+        """True / 1: multiplies report device times in their stats (and wait);
+        2: events only, read with last_timing() (multiplies do not wait)."""
+        check(self.lib.bt_ctx_set_timing(self.h, int(on)), "bt_ctx_set_timing")
+
+    def last_timing(self):
+        """(ms_numeric, ms_total) of the last multiply (timing mode 1 or 2)."""
+        a, b = C.c_double(), C.c_double()
+        check(self.lib.bt_ctx_last_timing(self.h, C.byref(a), C.byref(b)), "bt_ctx_last_timing")
+        return a.value, b.value
 
     @property
     def kernel_count(self) -> int:
