@@ -115,16 +115,22 @@ __device__ __forceinline__ int band_of(int64_t j, const RowArgs& g) {
 // lengths, and every thread takes flat pair indices (binary search into the
 // prefix), so all global loads of a chunk are independent (no per-k latency
 // chain).
-constexpr int kChunkA = 256;   // A entries staged per chunk (= blockDim)
-constexpr int kPairCap = 2048; // pairs staged per emission window (k_row_fill)
-constexpr int kPairPT = kPairCap / kChunkA;  // pairs per thread in the window sort
+// The symbolic kernels are instantiated for CH = 256 threads per row (long
+// rows: c1, c3, c5) and CH = 64 (short rows, many of them: c2, c4 -- four
+// times the rows in flight per SM).  CH A entries are staged per chunk
+// (= blockDim); emission windows hold kPairPT * CH pairs.
+constexpr int kChunkA = 256;   // the wide variant (host-side chunk arithmetic)
+constexpr int kPairPT = 8;     // pairs per thread in the window sort
+template <int CH>
+constexpr int pair_cap() { return kPairPT * CH; }
 
-struct RowChunk {  // shared-memory staging of up to kChunkA A entries
-  int32_t k[kChunkA];
-  int32_t b0[kChunkA];
-  int32_t pref[kChunkA + 1];
-  int32_t ksz[kChunkA];  // block size along k
-  int32_t au[kChunkA];   // T8 tile offset of the A block (offset / 64)
+template <int CH>
+struct RowChunk {  // shared-memory staging of up to CH A entries
+  int32_t k[CH];
+  int32_t b0[CH];
+  int32_t pref[CH + 1];
+  int32_t ksz[CH];  // block size along k
+  int32_t au[CH];   // T8 tile offset of the A block (offset / 64)
 };
 
 // first position in b_col[lo, hi) with column >= j (B rows are column sorted)
@@ -140,9 +146,10 @@ __device__ __forceinline__ int32_t col_lower_bound(const int32_t* __restrict__ c
 // Stage A entries [e0, e0 + kChunkA) of row i; returns the pair count of the
 // chunk.  Pairs are restricted to C columns [j0, j1) (the current column chunk;
 // the whole row when [0, ncols)).
-__device__ int64_t stage_chunk(const RowArgs& g, int32_t e0, int32_t e1, RowChunk& rc,
+template <int CH>
+__device__ int64_t stage_chunk(const RowArgs& g, int32_t e0, int32_t e1, RowChunk<CH>& rc,
                                int64_t j0, int64_t j1) {
-  using BS = cub::BlockScan<int32_t, kChunkA>;
+  using BS = cub::BlockScan<int32_t, CH>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int32_t total;
   const int32_t e = e0 + threadIdx.x;
@@ -164,7 +171,7 @@ __device__ int64_t stage_chunk(const RowArgs& g, int32_t e0, int32_t e1, RowChun
   BS(tmp).ExclusiveSum(len, ex, tot);
   rc.pref[threadIdx.x] = ex;
   if (threadIdx.x == 0) {
-    rc.pref[kChunkA] = tot;
+    rc.pref[CH] = tot;
     total = tot;
   }
   __syncthreads();
@@ -172,7 +179,8 @@ __device__ int64_t stage_chunk(const RowArgs& g, int32_t e0, int32_t e1, RowChun
 }
 
 // local A entry of flat pair t: last l with pref[l] <= t
-__device__ __forceinline__ int find_entry(const RowChunk& rc, int n, int32_t t) {
+template <int CH>
+__device__ __forceinline__ int find_entry(const RowChunk<CH>& rc, int n, int32_t t) {
   int lo = 0, hi = n;  // pref[lo] <= t < pref[hi]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -191,8 +199,9 @@ __device__ __forceinline__ int find_entry(const RowChunk& rc, int n, int32_t t) 
 // before / split_c0 (split fill CTAs): before[j] also counts the kept pairs of
 // the A entries ahead of split_c0 (the chunks of the earlier CTAs of the row).
 // Counters are local to the column chunk [j0, j0 + jw): cnt[j - j0].
+template <int CH>
 __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_t* bits,
-                             RowChunk& rc, unsigned long long* cand, unsigned long long* mnk,
+                             RowChunk<CH>& rc, unsigned long long* cand, unsigned long long* mnk,
                              int64_t j0, int64_t jw,
                              uint32_t* cache_j = nullptr, int32_t* cache_bu = nullptr,
                              uint32_t* before = nullptr, int32_t split_c0 = 0) {
@@ -210,10 +219,10 @@ __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
   }
   const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
   bool cached = false;
-  for (int32_t c0 = a0; c0 < a1; c0 += kChunkA) {
-    const int n = min(kChunkA, a1 - c0);
-    const int64_t T = stage_chunk(g, c0, a1, rc, j0, j0 + jw);
-    const bool cache = cache_j && a1 - a0 <= kChunkA && T <= kPairCap;
+  for (int32_t c0 = a0; c0 < a1; c0 += CH) {
+    const int n = min(CH, a1 - c0);
+    const int64_t T = stage_chunk<CH>(g, c0, a1, rc, j0, j0 + jw);
+    const bool cache = cache_j && a1 - a0 <= CH && T <= pair_cap<CH>();
     const bool ahead = before && c0 < split_c0;
     for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
       const int l = find_entry(rc, n, static_cast<int32_t>(t));
@@ -255,8 +264,9 @@ __device__ __forceinline__ unsigned long long agg_add(unsigned long long* ctr, i
 }
 
 // Touched columns of the row in ascending order -> tcol[0..n); returns n.
+template <int CH>
 __device__ int compact_touched(const uint32_t* bits, int nw, int32_t* tcol) {
-  using BS = cub::BlockScan<int, kChunkA>;
+  using BS = cub::BlockScan<int, CH>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ int total;
   int run = 0;
@@ -277,12 +287,13 @@ __device__ int compact_touched(const uint32_t* bits, int nw, int32_t* tcol) {
 
 // Pass 1: per C block-row i -- number of C_out blocks, products, T8 slab size,
 // stored elements, per-class work items, useful flops.
-__global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
+template <int CH>
+__global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
   extern __shared__ uint32_t cnt[];
   uint32_t* bits = cnt + g.colw;
   int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.colw + 31) >> 5));
   __shared__ unsigned long long cls_items[NSEG];
-  __shared__ RowChunk rc;
+  __shared__ RowChunk<CH> rc;
   const int64_t i = blockIdx.x;
   // empty C row (no A entries, no C_in blocks): sizes are zero, nothing else
   // (tensor-shaped operands such as c4 leave most matricized rows empty)
@@ -302,7 +313,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
   for (int64_t j0 = 0; j0 < g.ncols; j0 += g.colw) {
     const int64_t jw = min(g.colw, g.ncols - j0);
     row_products(g, i, cnt, bits, rc, &cand, &mnk, j0, jw);
-    const int ntouch = compact_touched(bits, static_cast<int>((jw + 31) >> 5), tcol);
+    const int ntouch = compact_touched<CH>(bits, static_cast<int>((jw + 31) >> 5), tcol);
     for (int q = threadIdx.x; q < ntouch; q += blockDim.x) {
       const int jl = tcol[q];
       const int64_t j = j0 + jl;
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
   }
   // the six row sums in one reduction: shuffles within each warp, one
   // barrier, then thread 0 adds the per-warp partials (exact integer sums)
-  constexpr int kW = kChunkA / 32;
+  constexpr int kW = CH / 32;
   __shared__ long long part[6][kW];
   long long r6[6] = {nnz, prods, vals, elems, static_cast<long long>(cand),
                      static_cast<long long>(mnk)};
@@ -367,16 +378,18 @@ __global__ void __launch_bounds__(kChunkA) k_row_count(const RowArgs g) {
 #ifndef BT_FILL_MINB
 #define BT_FILL_MINB 4
 #endif
-__global__ void __launch_bounds__(kChunkA, BT_FILL_MINB) k_row_fill(const RowArgs g) {
+template <int CH>
+__global__ void __launch_bounds__(CH, BT_FILL_MINB * 256 / CH) k_row_fill(const RowArgs g) {
+  constexpr int kPairCap = pair_cap<CH>();
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                                        // counts -> C entry rank
   int32_t* cur = reinterpret_cast<int32_t*>(sm + g.colw);  // product cursor
   uint32_t* bits = sm + 2 * g.colw;                         // touched columns
-  __shared__ RowChunk rc;
+  __shared__ RowChunk<CH> rc;
   __shared__ int32_t s_bu[kPairCap];  // B tile offset of staged pair
   __shared__ int16_t s_l[kPairCap];   // local A entry of staged pair
   __shared__ uint32_t s_key[kPairCap];  // sorted (column, slot) keys
-  using Sort = cub::BlockRadixSort<uint32_t, kChunkA, kPairPT>;
+  using Sort = cub::BlockRadixSort<uint32_t, CH, kPairPT>;
   __shared__ typename Sort::TempStorage sort_tmp;
   __shared__ unsigned long long cls_n[NSEG], cls_at[NSEG];
   // long rows: `splits` CTAs per row, CTA s emitting the products of its range
@@ -386,12 +399,12 @@ __global__ void __launch_bounds__(kChunkA, BT_FILL_MINB) k_row_fill(const RowArg
   const int split = static_cast<int>(blockIdx.x % g.splits);
   if (g.out_rp[i] == g.out_rp[i + 1]) return;  // empty C row: nothing to emit
   const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
-  const int nch = (a1 - a0 + kChunkA - 1) / kChunkA;
+  const int nch = (a1 - a0 + CH - 1) / CH;
   const int ch_lo = static_cast<int>((static_cast<int64_t>(split) * nch) / g.splits);
   const int ch_hi = static_cast<int>((static_cast<int64_t>(split + 1) * nch) / g.splits);
   if (split > 0 && ch_lo == ch_hi) return;
-  const int32_t e_lo = a0 + ch_lo * kChunkA;
-  const int32_t e_hi = min(a1, a0 + ch_hi * kChunkA);
+  const int32_t e_lo = a0 + ch_lo * CH;
+  const int32_t e_hi = min(a1, a0 + ch_hi * CH);
   uint32_t* before = nullptr;
   if (split > 0)
     before = sm + (g.colmask ? ((3 * g.colw + ((g.colw + 31) >> 5) + 1) & ~int64_t(1)) +
@@ -411,14 +424,14 @@ __global__ void __launch_bounds__(kChunkA, BT_FILL_MINB) k_row_fill(const RowArg
   // single-chunk rows: pair columns / B offsets cached, rc stays staged
   const bool cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, j0, jw, s_key, s_bu,
                                    before, e_lo);
-  const int ntouch = compact_touched(bits, static_cast<int>((jw + 31) >> 5), tcol);
+  const int ntouch = compact_touched<CH>(bits, static_cast<int>((jw + 31) >> 5), tcol);
   {
     // touched columns in ascending order, 256 at a time: ranks, product bases
     // and T8 offsets by block scans
     // both exclusive scans at once: warp shuffles, then the per-warp totals
     // through shared memory (2 barriers per 256 columns instead of two cub
     // block scans with their own barriers)
-    constexpr int kW = kChunkA / 32;
+    constexpr int kW = CH / 32;
     __shared__ long long wt[2][kW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int q0 = 0; q0 < ntouch; q0 += blockDim.x) {
@@ -485,9 +498,9 @@ __global__ void __launch_bounds__(kChunkA, BT_FILL_MINB) k_row_fill(const RowArg
       if (jl >= 0 && jl < jw) g.cin_map[cbase + cnt[jl]] = g.c_off[e];
     }
   // ---- products of this column chunk, k ascending (this CTA's A chunks)
-  for (int32_t c0 = e_lo; c0 < e_hi; c0 += kChunkA) {
-    const int n = min(kChunkA, a1 - c0);
-    const int64_t T = cached ? rc.pref[n] : stage_chunk(g, c0, a1, rc, j0, j0 + jw);
+  for (int32_t c0 = e_lo; c0 < e_hi; c0 += CH) {
+    const int n = min(CH, a1 - c0);
+    const int64_t T = cached ? rc.pref[n] : stage_chunk<CH>(g, c0, a1, rc, j0, j0 + jw);
     if (cached && g.colmask && n <= 64) {
       // rank emission from the cached pairs (no global loads in the sweeps)
       unsigned long long* mask = reinterpret_cast<unsigned long long*>(
@@ -988,6 +1001,18 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       fill_splits = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, chunks / 2)));
     }
     fill_splits = std::min(64, std::max(1, env_int("BT_FILL_SPLITS", fill_splits)));
+    // threads per row of the symbolic passes: 64 for many short rows (few A
+    // entries, few pairs: c2, c4 -- four times the rows in flight), else 256
+    const double a_per_row = M ? static_cast<double>(A.nblk) / static_cast<double>(M) : 0.0;
+    const double b_per_row = A.nbc ? static_cast<double>(B.nblk) / static_cast<double>(A.nbc) : 0.0;
+    // (and only while a row's column counters stay small: the 64-thread fill
+    // pays off with >= ~10 resident CTAs per SM -- c4 pass 1 165 -> 83 us,
+    // fill 229 -> 112 us; c2, whose 1 463-column counters take 29 KB, gains
+    // nothing, profiles/r02/row_threads_ab.txt)
+    int row_threads = (a_per_row <= 48.0 && a_per_row * b_per_row <= 384.0 &&
+                       M >= 2 * x.num_sms && row_smem <= 12 * 1024) ? 64 : 256;
+    row_threads = env_int("BT_ROW_THREADS", row_threads) == 64 ? 64 : 256;
+    if (row_threads == 64) fill_splits = 1;
     BT_REQUIRE(row_smem <= 180 * 1024, BT_ERR_INTERNAL, "multiply: column chunk too wide");
     // split CTAs need 4 more bytes per column; if that does not fit, one CTA
     // per row
@@ -1078,8 +1103,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     if (M > 0) {
       const size_t sm1 = static_cast<size_t>(W) * 8 + 4 * ((W + 31) / 32);
       // static + dynamic shared memory may exceed the 48 KB default: always opt in
-      ensure_dyn_smem(reinterpret_cast<const void*>(k_row_count), sm1);
-      k_row_count<<<static_cast<unsigned>(M), kChunkA, sm1, st>>>(ra);
+      auto count_fn = row_threads == 64 ? k_row_count<64> : k_row_count<256>;
+      ensure_dyn_smem(reinterpret_cast<const void*>(count_fn), sm1);
+      count_fn<<<static_cast<unsigned>(M), row_threads, sm1, st>>>(ra);
       check_launch("row_count");
       count_launch(&x);
     }
@@ -1168,8 +1194,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.nitems_total = nitems;
     if (phases) BT_CUDA(cudaEventRecord(x.ev[5], st));
     if (nout > 0) {
-      ensure_dyn_smem(reinterpret_cast<const void*>(k_row_fill), row_smem);
-      k_row_fill<<<static_cast<unsigned>(M * fill_splits), kChunkA, row_smem, st>>>(ra);
+      auto fill_fn = row_threads == 64 ? k_row_fill<64> : k_row_fill<256>;
+      ensure_dyn_smem(reinterpret_cast<const void*>(fill_fn), row_smem);
+      fill_fn<<<static_cast<unsigned>(M * fill_splits), row_threads, row_smem, st>>>(ra);
       check_launch("row_fill");
       count_launch(&x);
     }

@@ -442,3 +442,37 @@ def test_dfma_tiny_blocks(oracle, ctx, monkeypatch, case):
         assert_parity(from_store(c), want)
         # the DFMA output slots carry zero padding (norms read it)
         assert np.allclose(c.norms(), oracle.norms(want), rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("colmask,sort_min,colw", [(1, 48, 0), (0, 48, 0), (0, 0, 0),
+                                                   (0, 100000, 0), (1, 48, 50), (0, 0, 37)])
+def test_row_threads_64_vs_256(oracle, ctx, monkeypatch, colmask, sort_min, colw):
+    """The symbolic passes with 64 and with 256 threads per row (BT_ROW_THREADS):
+    against the oracle and bit-identical to each other, through every
+    emission path, column chunks, C_in and the eps filter.  Rows here hold up
+    to 300 A entries (several 64-entry chunks)."""
+    from paper_1910_13555_b200.store import multiply_local
+    monkeypatch.setenv("BT_COLMASK", str(colmask))
+    monkeypatch.setenv("BT_SORT_MIN", str(sort_min))
+    if colw:
+        monkeypatch.setenv("BT_COLW", str(colw))
+    rng = np.random.default_rng(64 + colw)
+    rsz = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 8)]
+    ksz = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 300)]
+    nsz = np.array([5, 13, 23, 4], np.int32)[rng.integers(0, 4, 120)]
+    A = _dense_rows(oracle, oracle.random_matrix(6401, rsz, ksz, 0.02), rsz, ksz, rng)
+    B = oracle.random_matrix(6402, ksz, nsz, 0.1)
+    Cin = oracle.random_matrix(6403, rsz, nsz, 0.2)
+    out = {}
+    for t in ("64", "256"):
+        monkeypatch.setenv("BT_ROW_THREADS", t)
+        for eps in (0.0, 30.0):
+            want, nprod, _ = oracle.multiply(A, B, Cin, eps)
+            a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+            st = multiply_local(ctx, a, b, c, eps)
+            assert st["products"] == nprod
+            got = from_store(c)
+            assert_parity(got, want)
+            out[(t, eps)] = got
+    for eps in (0.0, 30.0):
+        assert np.array_equal(out[("64", eps)].vals, out[("256", eps)].vals)
