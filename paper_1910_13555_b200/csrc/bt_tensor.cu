@@ -23,6 +23,9 @@
 namespace bt {
 
 constexpr int kMaxRank = 4;
+#ifndef BT_REMAP_U
+#define BT_REMAP_U 4
+#endif
 
 struct TensorMap {
   int ndim;
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(128) k_remap_vals(
   const int step = blockDim.x >> 6;
   // four tiles per thread and sweep: the four gathers are issued together
   // (the kernel is bound by gather latency, ncu: long-scoreboard stalls)
-  constexpr int U = 4;
+  constexpr int U = BT_REMAP_U;
   for (int t0 = threadIdx.x >> 6; t0 < ntiles; t0 += U * step) {
     double v[U];
 #pragma unroll
