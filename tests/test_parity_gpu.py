@@ -476,3 +476,38 @@ def test_row_threads_64_vs_256(oracle, ctx, monkeypatch, colmask, sort_min, colw
             out[(t, eps)] = got
     for eps in (0.0, 30.0):
         assert np.array_equal(out[("64", eps)].vals, out[("256", eps)].vals)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_sweep(oracle, ctx, seed):
+    """Randomised configurations against the oracle: block sizes 1..40 drawn
+    per dimension from a random palette (tiny DFMA, DMMA tile classes, tall
+    rows, generic n > 32), random shapes, occupancies, C_in, eps (with scaled
+    values so the filter bites)."""
+    from paper_1910_13555_b200.store import multiply_local
+    rng = np.random.default_rng(1000 + seed)
+
+    def sizes(n):
+        pal = rng.choice(np.arange(1, 41), size=int(rng.integers(1, 5)), replace=False)
+        if rng.random() < 0.2:
+            pal = np.append(pal, rng.choice([169, 299]))   # tall (rows only below)
+        return pal.astype(np.int32), int(n)
+
+    pm, nm = sizes(rng.integers(1, 30))
+    pk, nk = sizes(rng.integers(1, 40))
+    pn, nn = sizes(rng.integers(1, 30))
+    rsz = rng.choice(pm, nm).astype(np.int32)
+    ksz = rng.choice(pk[pk <= 64] if np.any(pk <= 64) else [8], nk).astype(np.int32)
+    nsz = rng.choice(pn[pn <= 40] if np.any(pn <= 40) else [8], nn).astype(np.int32)
+    scale = float(rng.choice([0.0, 6.0]))
+    oa, ob, oc = (float(rng.choice([0.05, 0.2, 0.5, 1.0])) for _ in range(3))
+    A = oracle.random_matrix(2000 + seed, rsz, ksz, oa, scale)
+    B = oracle.random_matrix(3000 + seed, ksz, nsz, ob, scale)
+    Cin = oracle.random_matrix(4000 + seed, rsz, nsz, oc * float(rng.random() < 0.5), scale)
+    eps = float(rng.choice([0.0, 1e-6, 1e-3])) if scale else 0.0
+    want, nprod, flops = oracle.multiply(A, B, Cin, eps)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    st = multiply_local(ctx, a, b, c, eps)
+    assert st["products"] == nprod
+    assert st["flops"] == flops
+    assert_parity(from_store(c), want)
