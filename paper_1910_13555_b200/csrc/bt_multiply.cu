@@ -1356,7 +1356,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         g.nitems = hi - lo;
         g.counter = counters + q;
         if (q == GENERIC) {
-          k_smm_generic<<<static_cast<unsigned>(hi - lo), 128, 0, ks>>>(g);
+          k_smm_generic<<<static_cast<unsigned>(hi - lo), 256, 0, ks>>>(g, A.csz.p);
           check_launch("smm_generic");
           count_launch(&x);
           continue;

@@ -507,37 +507,92 @@ __global__ void __launch_bounds__(128) k_smm_dfma(const NumArgs g, const int32_t
   }
 }
 
-// Generic small-GEMM (n > 32 or k > 64): one CTA per C block, one thread per
-// element, T8 operands, products in k order.  Every position of the T8 slot is
-// written -- the padding with zeros -- because the output slab is not cleared
-// beforehand and norms, the eps filter and later DMMA reads of this block as an
-// operand all rely on zero padding.
-__global__ void k_smm_generic(const NumArgs g) {
+// Generic small-GEMM for blocks the DMMA tile kernels do not take (n > 32 or
+// k > 64): one CTA of 256 threads per C block, the block swept in 64 x 64
+// output sub-tiles, each thread owning a 4 x 4 register micro-tile
+// (CUDA-core DFMA).  Per product, k is walked in chunks of 16: the 64 x 16
+// A panel and 16 x 64 B panel are gathered from the T8 slots into shared
+// memory (padding outside the block as zeros), then every k step is 4 A and
+// 4 B shared-memory reads for 16 DFMAs.  Products in ascending k per C
+// element (block.hpp:45-60 order); the whole T8 slot is written, padding as
+// zeros (norms, the eps filter and DMMA reads of this block as an operand
+// rely on zero padding).
+constexpr int kGenT = 64;   // output sub-tile edge
+constexpr int kGenK = 16;   // k chunk
+__global__ void __launch_bounds__(256) k_smm_generic(const NumArgs g, const int32_t* __restrict__ k_sz) {
+  __shared__ __align__(16) double sA[kGenK][kGenT + 2];  // [k][row] (+2: 16-byte rows)
+  __shared__ __align__(16) double sB[kGenK][kGenT + 2];  // [k][col]
   const int64_t id = g.item_lo + blockIdx.x;
   if (blockIdx.x >= g.nitems) return;
   const Item it = g.items[id];
   const int m = it.rows, n = it.n;
   const int NT = tiles8(n), MT = tiles8(m);
+  const int MP = MT * 8, NP = NT * 8;  // padded extents of the slot
   const int64_t p0 = item_p0(it);
-  const int padded = MT * 8 * NT * 8;
-  for (int e = threadIdx.x; e < padded; e += blockDim.x) {
-    const int r = e / (NT * 8), q = e - r * (NT * 8);
-    const int64_t cp = t8_pos(r, q, NT);
-    BT_DASSERT(it.c_off + cp < g.cout_len, "generic C range");
-    if (r >= m || q >= n) {
-      g.cout[it.c_off + cp] = 0.0;
-      continue;
+  const int t = threadIdx.x;
+  const int tr = (t >> 4) * 4, tc = (t & 15) * 4;  // this thread's micro-tile
+  for (int r0 = 0; r0 < MP; r0 += kGenT)
+    for (int c0 = 0; c0 < NP; c0 += kGenT) {
+      double acc[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int r = r0 + tr + u, c = c0 + tc + v;
+          acc[u][v] = (it.cin_off >= 0 && r < m && c < n) ? g.cin[it.cin_off + t8_pos(r, c, NT)]
+                                                          : 0.0;
+        }
+      for (int p = 0; p < it.np; ++p) {
+        const Desc d = g.desc[p0 + p];
+        const int k = k_sz[d.w];
+        const int KT = (d.z + 1) >> 1;
+        const double* A = g.at + static_cast<int64_t>(d.x) * 64;
+        const double* B = g.bt + static_cast<int64_t>(d.y) * 64;
+        BT_DASSERT(static_cast<int64_t>(d.x) * 64 + static_cast<int64_t>(MT) * KT * 64 <= g.a_len,
+                   "generic A range");
+        BT_DASSERT(static_cast<int64_t>(d.y) * 64 + static_cast<int64_t>(KT) * NT * 64 <= g.b_len,
+                   "generic B range");
+        for (int k0 = 0; k0 < k; k0 += kGenK) {
+          __syncthreads();  // the previous chunk's reads are done
+          // gather the A panel (64 rows x 16 k) and the B panel (16 k x 64 cols)
+          for (int e = t; e < kGenT * kGenK; e += 256) {
+            const int kk = e % kGenK, rr = e / kGenK;     // A: k fastest (T8 rows)
+            const int r = r0 + rr, kc = k0 + kk;
+            sA[kk][rr] = (r < m && kc < k) ? A[t8_pos(r, kc, KT)] : 0.0;
+            const int cc = e % kGenT, kb = e / kGenT;     // B: columns fastest
+            const int c = c0 + cc, kr = k0 + kb;
+            sB[kb][cc] = (c < n && kr < k) ? B[t8_pos(kr, c, NT)] : 0.0;
+          }
+          __syncthreads();
+          const int kn = min(kGenK, k - k0);
+          for (int kk = 0; kk < kn; ++kk) {
+            double a[4], b[4];  // 16-byte shared-memory reads (two per operand)
+            const double2 a01 = *reinterpret_cast<const double2*>(&sA[kk][tr]);
+            const double2 a23 = *reinterpret_cast<const double2*>(&sA[kk][tr + 2]);
+            const double2 b01 = *reinterpret_cast<const double2*>(&sB[kk][tc]);
+            const double2 b23 = *reinterpret_cast<const double2*>(&sB[kk][tc + 2]);
+            a[0] = a01.x; a[1] = a01.y; a[2] = a23.x; a[3] = a23.y;
+            b[0] = b01.x; b[1] = b01.y; b[2] = b23.x; b[3] = b23.y;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+          }
+        }
+      }
+      // store the sub-tile: padding positions of the slot as zeros
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int r = r0 + tr + u, c = c0 + tc + v;
+          if (r < MP && c < NP) {
+            const int64_t cp = t8_pos(r, c, NT);
+            BT_DASSERT(it.c_off + cp < g.cout_len, "generic C range");
+            g.cout[it.c_off + cp] = (r < m && c < n) ? acc[u][v] : 0.0;
+          }
+        }
     }
-    double acc = it.cin_off >= 0 ? g.cin[it.cin_off + cp] : 0.0;
-    for (int p = 0; p < it.np; ++p) {
-      const Desc d = g.desc[p0 + p];
-      const int KT = (d.z + 1) >> 1;
-      const double* a = g.at + static_cast<int64_t>(d.x) * 64;
-      const double* b = g.bt + static_cast<int64_t>(d.y) * 64;
-      for (int c = 0; c < 4 * d.z; ++c) acc = fma(a[t8_pos(r, c, KT)], b[t8_pos(c, q, NT)], acc);
-    }
-    g.cout[it.c_off + cp] = acc;
-  }
 }
 
 }  // namespace bt

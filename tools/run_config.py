@@ -66,6 +66,15 @@ def config(name, rng, occ=None):
         M = blocks_random(rng, aux, aux, 0.0, band=7)
         return rows, aux, aux, T, M, 0.0, ("c4: (ab|P)(P|Q), a,b 200 AO blocks, P,Q 400 aux "
                                            "blocks, 13/23 alternating, T occ 0.001, (P|Q) band 7")
+    if name in ("big64", "big40"):
+        # not a BASELINE config: blocks wider than the DMMA tile kernels take
+        # (n > 32): the generic kernel's workload
+        bs = int(name[3:])
+        sz = np.full(200, bs, np.int32)
+        o = 0.1 if occ is None else occ
+        A = blocks_random(rng, sz, sz, o)
+        B = blocks_random(rng, sz, sz, o)
+        return sz, sz, sz, A, B, 0.0, f"{name}: 200x200 blocks of {bs}x{bs}, occ {o}"
     if name in ("tiny5", "tiny3", "tiny1"):
         # not a BASELINE config: uniform tiny blocks, ~20 products per C block
         # (compute-heavy), the DFMA-vs-DMMA A/B workload (BT_DFMA=0/1)
