@@ -107,6 +107,11 @@ struct RowArgs {
 };
 
 __device__ __forceinline__ int band_of(int64_t j, const RowArgs& g) {
+  if (g.nbands == 1) return 0;
+  // 32-bit division (j * nbands < 2^31 for any N the stores allow with <= 8 bands
+  // below 2^28 columns); the 64-bit one costs ~70 instructions per call
+  if (g.ncols < (int64_t(1) << 27))
+    return static_cast<int>(static_cast<uint32_t>(j * g.nbands) / static_cast<uint32_t>(g.ncols));
   return static_cast<int>((j * g.nbands) / g.ncols);
 }
 
@@ -204,6 +209,7 @@ __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
                              RowChunk<CH>& rc, unsigned long long* cand, unsigned long long* mnk,
                              int64_t j0, int64_t jw,
                              uint32_t* cache_j = nullptr, int32_t* cache_bu = nullptr,
+                             int16_t* cache_l = nullptr,
                              uint32_t* before = nullptr, int32_t split_c0 = 0) {
   const int nw = static_cast<int>((jw + 31) >> 5);
   for (int64_t j = threadIdx.x; j < jw; j += blockDim.x) cnt[j] = 0u;
@@ -236,6 +242,7 @@ __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
       if (cache) {
         cache_j[t] = static_cast<uint32_t>(j);
         cache_bu[t] = static_cast<int32_t>(g.b_off[f] >> 6);
+        cache_l[t] = static_cast<int16_t>(l);  // the emission sweeps skip the search
       }
       if (atomicAdd(&cnt[j], 1u) == 0u) atomicOr(&bits[j >> 5], 1u << (j & 31));
       if (ahead) atomicAdd(&before[j], 1u);
@@ -423,7 +430,7 @@ __global__ void __launch_bounds__(CH, BT_FILL_MINB * 256 / CH) k_row_fill(const 
   const int64_t jw = min(g.colw, g.ncols - j0);
   // single-chunk rows: pair columns / B offsets cached, rc stays staged
   const bool cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, j0, jw, s_key, s_bu,
-                                   before, e_lo);
+                                   s_l, before, e_lo);
   const int ntouch = compact_touched<CH>(bits, static_cast<int>((jw + 31) >> 5), tcol);
   {
     // touched columns in ascending order, 256 at a time: ranks, product bases
@@ -510,14 +517,13 @@ __global__ void __launch_bounds__(CH, BT_FILL_MINB * 256 / CH) k_row_fill(const 
       for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
         const uint32_t j = s_key[t];
         if (j == 0xffffffffu) continue;
-        const int l = find_entry(rc, n, static_cast<int32_t>(t));
-        atomicOr(&mask[j], 1ull << l);
+        atomicOr(&mask[j], 1ull << s_l[t]);
       }
       __syncthreads();
       for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
         const uint32_t j = s_key[t];
         if (j == 0xffffffffu) continue;
-        const int l = find_entry(rc, n, static_cast<int32_t>(t));
+        const int l = s_l[t];
         const int32_t p = cur[j] + __popcll(mask[j] & ((1ull << l) - 1ull));
         BT_DASSERT(p >= 0 && pbase + p < g.prod_base[i + 1], "descriptor slot");
         g.desc[pbase + p] = make_int4(rc.au[l], s_bu[t], (rc.ksz[l] + 3) >> 2, rc.k[l]);
