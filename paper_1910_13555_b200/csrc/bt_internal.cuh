@@ -128,6 +128,7 @@ struct Ctx {
   // results there directly, so reading them back needs no copy-engine D2H --
   // which would queue behind an asynchronous export's bulk transfer
   void* pinned_dev = nullptr;
+  unsigned long long size_seq = 0;  // sequence of the multiply's sizes flag (pinned + 3072)
   // Grow-only pinned host staging for index uploads: one packed H2D per call
   // instead of several pageable copies.  stage_ev marks the last copy that read
   // it; host_stage() waits for it before handing the buffer out again.

@@ -16,6 +16,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <tuple>
 #include <mutex>
 #include <map>
@@ -772,6 +773,16 @@ __device__ void init_cursors(const unsigned long long* __restrict__ seg_items,
 // scanned across the CTA in one pass (warp shuffles, then the 32 warp totals
 // by warp 0), and it writes its rows' prefixes -- two barriers in all (the
 // three CUB block scans per 1 024 rows took 8-15 us, spilling).
+// The sizes block lives in mapped page-locked memory; once all of it is
+// written, thread 0 publishes `seq` in `ready` (system-scope fence first), so
+// the host can poll that word instead of waiting for the stream.
+__device__ __forceinline__ void publish_sizes(volatile unsigned long long* ready,
+                                              unsigned long long seq) {
+  __threadfence_system();  // every writer's sizes visible to the host ...
+  __syncthreads();
+  if (threadIdx.x == 0 && ready) *ready = seq;  // ... before the flag
+}
+
 __global__ void __launch_bounds__(1024) k_scan_rows(const int32_t* __restrict__ nnz,
                                                     const int64_t* __restrict__ prod,
                                                     const int64_t* __restrict__ vals, int64_t M,
@@ -781,7 +792,9 @@ __global__ void __launch_bounds__(1024) k_scan_rows(const int32_t* __restrict__ 
                                                     const unsigned long long* __restrict__ tot,
                                                     int ntot,
                                                     unsigned long long* __restrict__ sizes,
-                                                    unsigned long long* __restrict__ cursor) {
+                                                    unsigned long long* __restrict__ cursor,
+                                                    volatile unsigned long long* ready,
+                                                    unsigned long long seq) {
   __shared__ long long wsum[3][32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int per = static_cast<int>((M + 1023) / 1024);
@@ -849,6 +862,7 @@ __global__ void __launch_bounds__(1024) k_scan_rows(const int32_t* __restrict__ 
   }
   for (int q = t; q < ntot; q += blockDim.x) sizes[3 + q] = tot[q];
   init_cursors(tot + 3, cursor);
+  publish_sizes(ready, seq);
 }
 
 // Large-M variant of the readback block (after the CUB scans).
@@ -856,7 +870,8 @@ __global__ void k_pack_sizes(const int32_t* __restrict__ rp, const int64_t* __re
                              const int64_t* __restrict__ vb, int64_t M,
                              const unsigned long long* __restrict__ tot, int ntot,
                              unsigned long long* __restrict__ sizes,
-                             unsigned long long* __restrict__ cursor) {
+                             unsigned long long* __restrict__ cursor,
+                             volatile unsigned long long* ready, unsigned long long seq) {
   if (threadIdx.x == 0) {
     sizes[0] = static_cast<unsigned long long>(rp[M]);
     sizes[1] = static_cast<unsigned long long>(pb[M]);
@@ -864,6 +879,7 @@ __global__ void k_pack_sizes(const int32_t* __restrict__ rp, const int64_t* __re
   }
   for (int t = threadIdx.x; t < ntot; t += blockDim.x) sizes[3 + t] = tot[t];
   init_cursors(tot + 3, cursor);
+  publish_sizes(ready, seq);
 }
 
 // ------------------------------------------------------------------- host
@@ -1143,6 +1159,13 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     // page-locked memory (a copy-engine D2H would queue behind an
     // asynchronous export's transfer)
     unsigned long long* dsizes = reinterpret_cast<unsigned long long*>(x.pinned_dev);
+    // the scan kernel publishes `seq` in this mapped word once the sizes are in
+    // place: the host polls it (no stream-synchronize wake-up latency)
+    volatile unsigned long long* ready_host = reinterpret_cast<volatile unsigned long long*>(
+        static_cast<char*>(x.pinned) + 3072);
+    volatile unsigned long long* ready_dev = reinterpret_cast<volatile unsigned long long*>(
+        static_cast<char*>(x.pinned_dev) + 3072);
+    const unsigned long long seq = ++x.size_seq;
     unsigned long long* cursor = x.ws<unsigned long long>(18, NSEG + NCLASS);
     ra.row_nnz = row_nnz;
     ra.row_prod = row_prod;
@@ -1160,7 +1183,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     }
     if (M <= 8192) {
       k_scan_rows<<<1, 1024, 0, st>>>(row_nnz, row_prod, row_vals, M, out_rp.p, prod_base,
-                                      val_base, tot, 3 + NSEG, dsizes, cursor);
+                                      val_base, tot, 3 + NSEG, dsizes, cursor, ready_dev, seq);
       check_launch("scan_rows");
       count_launch(&x);
     } else {
@@ -1171,7 +1194,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       exclusive_scan(x, row_prod, prod_base, M + 1);
       exclusive_scan(x, row_vals, val_base, M + 1);
       k_pack_sizes<<<1, 256, 0, st>>>(out_rp.p, prod_base, val_base, M, tot, 3 + NSEG, dsizes,
-                                      cursor);
+                                      cursor, ready_dev, seq);
       check_launch("pack_sizes");
       count_launch(&x);
     }
@@ -1185,7 +1208,19 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     const bool phases = x.timing && env_int("BT_PHASES", 0);
     if (phases) BT_CUDA(cudaEventRecord(x.ev[4], st));
     tr.mark("pass1 enqueued");
-    BT_CUDA(cudaStreamSynchronize(st));
+    if (M > 0 && env_int("BT_POLL_SIZES", 1)) {
+      // poll the flag; after 20 ms fall back to the stream wait (which also
+      // reports a failed kernel)
+      const double t_start = Trace::now();
+      unsigned spins = 0;
+      while (*ready_host != seq) {
+        if ((++spins & 4095u) == 0 && Trace::now() - t_start > 20.0) break;
+      }
+      if (*ready_host != seq) BT_CUDA(cudaStreamSynchronize(st));
+      std::atomic_thread_fence(std::memory_order_acquire);
+    } else {
+      BT_CUDA(cudaStreamSynchronize(st));
+    }
     tr.mark("pass1 sync");
     // caller's check between the sizes and any use of B's values (the
     // speculative case-2 gather confirms its segments here, or throws)
