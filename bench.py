@@ -221,6 +221,9 @@ def relaunch_under_torchrun(n: int):
     if env.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
         env["NCCL_DEBUG"] = "INFO"          # the communicator init lines (ranks, NVLink)
         env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # to stderr: stdout's last line stays the JSON line (NCCL's teardown
+        # messages of the other ranks would otherwise follow it)
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.abspath(__file__)] + sys.argv[1:]

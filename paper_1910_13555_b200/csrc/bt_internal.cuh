@@ -123,12 +123,19 @@ struct Ctx {
   int64_t kernels = 0;  // kernels launched through this context
   void* nccl = nullptr; // ncclComm_t when nranks > 1
   DBuf<unsigned char> scratch;  // CUB temp storage, reused
-  void* pinned = nullptr;       // small pinned host staging for scalar readbacks
+  // small mapped page-locked staging for scalar readbacks; layout (bytes):
+  //   [0, 1200)      the multiply's sizes block / the export's chunk offsets
+  //   [512, 3072)    exchange headers (bt_dist.cu, word 64 on; used between
+  //                  multiplies, never while a sizes block is pending)
+  //   [3072, ...)    the B-gather size headers (word 384 on, 8 + 3P words)
+  //   [kPinnedFlag]  the multiply's sizes-ready flag (last 64 bytes)
+  static constexpr size_t kPinnedBytes = 8192, kPinnedFlag = kPinnedBytes - 64;
+  void* pinned = nullptr;
   // device alias of `pinned` (mapped page-locked memory): kernels write small
   // results there directly, so reading them back needs no copy-engine D2H --
   // which would queue behind an asynchronous export's bulk transfer
   void* pinned_dev = nullptr;
-  unsigned long long size_seq = 0;  // sequence of the multiply's sizes flag (pinned + 3072)
+  unsigned long long size_seq = 0;  // sequence of the multiply's sizes flag (kPinnedFlag)
   // Grow-only pinned host staging for index uploads: one packed H2D per call
   // instead of several pageable copies.  stage_ev marks the last copy that read
   // it; host_stage() waits for it before handing the buffer out again.

@@ -1162,9 +1162,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     // the scan kernel publishes `seq` in this mapped word once the sizes are in
     // place: the host polls it (no stream-synchronize wake-up latency)
     volatile unsigned long long* ready_host = reinterpret_cast<volatile unsigned long long*>(
-        static_cast<char*>(x.pinned) + 3072);
+        static_cast<char*>(x.pinned) + Ctx::kPinnedFlag);
     volatile unsigned long long* ready_dev = reinterpret_cast<volatile unsigned long long*>(
-        static_cast<char*>(x.pinned_dev) + 3072);
+        static_cast<char*>(x.pinned_dev) + Ctx::kPinnedFlag);
     const unsigned long long seq = ++x.size_seq;
     unsigned long long* cursor = x.ws<unsigned long long>(18, NSEG + NCLASS);
     ra.row_nnz = row_nnz;

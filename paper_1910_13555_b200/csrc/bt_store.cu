@@ -469,7 +469,7 @@ static bt_ctx* new_ctx(int device) {
   BT_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t thr = UINT64_MAX;
   BT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-  BT_CUDA(cudaHostAlloc(&x.pinned, 4096, cudaHostAllocMapped));
+  BT_CUDA(cudaHostAlloc(&x.pinned, Ctx::kPinnedBytes, cudaHostAllocMapped));
   BT_CUDA(cudaHostGetDevicePointer(&x.pinned_dev, x.pinned, 0));
   BT_CUDA(cudaEventCreateWithFlags(&x.stage_ev, cudaEventDisableTiming));
   for (auto& e : x.ev) BT_CUDA(cudaEventCreate(&e));
