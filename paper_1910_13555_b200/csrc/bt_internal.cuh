@@ -159,6 +159,7 @@ struct Ctx {
   // later export compacts into b only after it (asynchronous exports,
   // bt_mat_export_async, leave the main stream free meanwhile).
   DBuf<double> xstage[2];
+  cudaStream_t xfer = nullptr;  // the export's D2H stream (not shared with kernels)
   cudaEvent_t xfer_done[2] = {nullptr, nullptr};
   int xnext = 0;
   // waits for every stream of the context (main + side streams)

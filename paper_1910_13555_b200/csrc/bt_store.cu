@@ -67,6 +67,7 @@ void Ctx::sync_all() {
   BT_CUDA(cudaStreamSynchronize(stream));
   for (auto& a : aux)
     if (a) BT_CUDA(cudaStreamSynchronize(a));
+  if (xfer) BT_CUDA(cudaStreamSynchronize(xfer));
 }
 
 unsigned char* Ctx::host_stage(size_t bytes) {
@@ -474,6 +475,7 @@ static bt_ctx* new_ctx(int device) {
   BT_CUDA(cudaEventCreateWithFlags(&x.stage_ev, cudaEventDisableTiming));
   for (auto& e : x.ev) BT_CUDA(cudaEventCreate(&e));
   for (auto& a : x.aux) BT_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+  BT_CUDA(cudaStreamCreateWithFlags(&x.xfer, cudaStreamNonBlocking));
   BT_CUDA(cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming));
   for (auto& e : x.xfer_done) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : x.ev_join) BT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -539,7 +541,8 @@ int bt_ctx_destroy(bt_ctx* c) {
     cudaSetDevice(x.device);
     cudaStreamSynchronize(x.stream);
     for (auto& a : x.aux)
-      if (a) cudaStreamSynchronize(a);  // asynchronous exports still in flight
+      if (a) cudaStreamSynchronize(a);
+    if (x.xfer) cudaStreamSynchronize(x.xfer);  // asynchronous exports still in flight
     for (auto& b : x.xstage) b.release();
     for (auto& e : x.xfer_done)
       if (e) cudaEventDestroy(e);
@@ -554,6 +557,7 @@ int bt_ctx_destroy(bt_ctx* c) {
       if (e) cudaEventDestroy(e);
     for (auto& a : x.aux)
       if (a) cudaStreamDestroy(a);
+    if (x.xfer) cudaStreamDestroy(x.xfer);
     if (x.ev_fork) cudaEventDestroy(x.ev_fork);
     for (auto& e : x.ev_join)
       if (e) cudaEventDestroy(e);
@@ -915,7 +919,10 @@ static void export_store(const Mat& m, int64_t* bi, int64_t* bj, double* vals, b
         double* dst = x.xstage[xb].p;
         int64_t eo[kChunks + 1];
         for (int c = 0; c <= kChunks; ++c) eo[c] = meta_co[c];
-        cudaStream_t cs = x.aux[0];
+        // the value D2H runs on the context's transfer stream: kernels of
+        // later calls (side-stream numeric launches use aux[]) never queue
+        // behind an asynchronous export
+        cudaStream_t cs = x.xfer;
         for (int c = 0; c < kChunks; ++c) {
           if (cb[c + 1] == cb[c]) continue;
           k_compact<<<static_cast<unsigned>(cb[c + 1] - cb[c]), 128, 0, st>>>(
