@@ -282,9 +282,14 @@ void upload_parts(Ctx& x, const HostPart* parts, int n, void* const* dst);
 // sync_at_end: wait for the numeric phase before returning (the distributed
 // drivers rely on it); the single-GPU C-ABI call returns right after enqueuing
 // (stream-ordered: every later call on the context sees the finished C).
+// poll_sizes: wait for the pass-1 sizes by polling a mapped flag instead of a
+// stream synchronize -- single-GPU calls only: next to in-flight NCCL
+// transfers (Cannon shifts) the spinning host thread cost 1 s of a 1.4 s c5
+// Cannon multiply on 4 GPUs (profiles/r02/README.md).
 void local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& C, double eps, bt_stats* stats,
                     cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr,
-                    const std::function<void()>* after_sizes = nullptr, bool sync_at_end = true);
+                    const std::function<void()>* after_sizes = nullptr, bool sync_at_end = true,
+                    bool poll_sizes = false);
 
 }  // namespace bt
 

@@ -1028,7 +1028,8 @@ using namespace bt;
 // The local multiply C += A*B (one rank's stores); throws bt::Error.
 void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps, bt_stats* stats,
                         cudaEvent_t wait_numeric, cudaEvent_t numeric_start,
-                        const std::function<void()>* after_sizes, bool sync_at_end) {
+                        const std::function<void()>* after_sizes, bool sync_at_end,
+                        bool poll_sizes) {
   {
     BT_REQUIRE(A.ctx == &x && B.ctx == &x && Cm.ctx == &x, BT_ERR_INVALID_ARGUMENT,
                "bt_multiply: matrices belong to another context");
@@ -1208,7 +1209,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     const bool phases = x.timing && env_int("BT_PHASES", 0);
     if (phases) BT_CUDA(cudaEventRecord(x.ev[4], st));
     tr.mark("pass1 enqueued");
-    if (M > 0 && env_int("BT_POLL_SIZES", 1)) {
+    const int poll_mode = env_int("BT_POLL_SIZES", 1);  // 0 off, 1 single-GPU calls, 2 all
+    if (M > 0 && ((poll_sizes && poll_mode == 1) || poll_mode == 2)) {
       // poll the flag; after 20 ms fall back to the stream wait (which also
       // reports a failed kernel)
       const double t_start = Trace::now();
@@ -1519,7 +1521,7 @@ extern "C" int bt_multiply(bt_ctx* ctx, const bt_mat* ah, const bt_mat* bh, bt_m
   return guard([&] {
     BT_REQUIRE(ctx && ah && bh && ch, BT_ERR_INVALID_ARGUMENT, "null argument");
     local_multiply(ctx->impl, ah->impl, bh->impl, ch->impl, eps, stats, nullptr, nullptr, nullptr,
-                   false);
+                   false, ctx->impl.nranks == 1);
   });
 }
 
