@@ -990,6 +990,19 @@ int dmma_occupancy(KernelFn fn, size_t smem) {
   return per_sm;
 }
 
+// Tickets per atomic of the numeric kernels.  Short items (about one product
+// per C tile: c2, c4) are bound by the single ticket counter -- batches of up
+// to 8 (about 8 batches per warp, so the tail stays short): c2 numeric 0.121
+// -> 0.109 ms, c4 3.12 -> 2.93 ms.  Longer product chains (c1, c3) lose with
+// batches (c1 0.619 -> 0.684 ms at 8: neighbouring tiles move to one warp), so
+// they keep one ticket per item.  BT_TICKET_BATCH overrides.
+int ticket_batch(int64_t tickets, int64_t warps, double products_per_ticket) {
+  int64_t b = 1;
+  if (products_per_ticket < 2.0 && warps > 0)
+    b = std::max<int64_t>(1, std::min<int64_t>(8, tickets / (warps * 8)));
+  return std::max(1, std::min(64, env_int("BT_TICKET_BATCH", static_cast<int>(b))));
+}
+
 struct Plan {
   int stages = 1;
   int stage_doubles = 0;
@@ -1383,6 +1396,10 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
         const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,
                                                (hi - lo + kWarps - 1) / kWarps);
+        // K panels in one launch: one ticket per atomic -- batches let a warp
+        // hold tickets of a later panel while it waits on the earlier one
+        // (c3 10 %: 1.73 -> 2.81 ms with batches of 6)
+        g.ticket_batch = 1;
         fn<<<static_cast<unsigned>(grid), kWarps * 32, P.smem, st>>>(g);
         check_launch("smm_dmma_panels");
         count_launch(&x);
@@ -1427,6 +1444,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
         const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,
                                                (g.nitems + kWarps - 1) / kWarps);
+        g.ticket_batch = ticket_batch(g.nitems, grid * kWarps,
+                                      static_cast<double>(nprod) / std::max<int64_t>(nitems, 1));
         fn<<<static_cast<unsigned>(grid), kWarps * 32, smem, x.aux[0]>>>(g);
         check_launch("smm_dmma_multi");
         count_launch(&x);
@@ -1464,6 +1483,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         BT_REQUIRE(per_sm >= 1, BT_ERR_INTERNAL, "smm_dmma: kernel does not fit on an SM");
         const int64_t grid = std::min<int64_t>(static_cast<int64_t>(x.num_sms) * per_sm,
                                                (hi - lo + kWarps - 1) / kWarps);
+        g.ticket_batch = ticket_batch(g.nitems, grid * kWarps,
+                                      static_cast<double>(nprod) / std::max<int64_t>(nitems, 1));
         fn<<<static_cast<unsigned>(grid), kWarps * 32, P.smem, ks>>>(g);
         check_launch("smm_dmma");
         count_launch(&x);

@@ -60,6 +60,9 @@ struct NumArgs {
   int* tile_flag;
   // slab lengths in doubles (device checks of the checked build)
   int64_t a_len, b_len, cin_len, cout_len;
+  // tickets are drawn from `counter` in batches of this many consecutive
+  // items (>= 1): one global atomic per batch instead of per item
+  int ticket_batch;
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -134,13 +137,36 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
     return items + p * g.panel_stride + (id - p * g.nitems);
   };
 
+  // ---- ticket source (lane 0): batches of TB consecutive tickets, the next
+  // batch's base drawn one batch ahead so its atomic latency is hidden.  One
+  // global counter hit per item was the top stall of small-block multiplies
+  // (c2: 36 % of all warp stall samples on the atomicAdd, ncu).  A warp still
+  // works its tickets in increasing order (the K-panel deadlock argument holds).
+  const unsigned long long TB = g.ticket_batch > 1 ? static_cast<unsigned long long>(g.ticket_batch) : 1ull;
+  unsigned long long b_next = 0, b_end = 0, b_pre = 0;
+  // (MULTI instantiations only -- the small-block launches; single-class
+  // launches keep one ticket per item and none of this state: with it the
+  // c1 kernel went 0.591 -> 0.623 ms at batch 1)
+  auto draw = [&]() -> unsigned long long {
+    if constexpr (!MULTI) {
+      return atomicAdd(g.counter, 1ull);
+    } else {
+      if (b_next == b_end) {
+        b_next = b_pre;
+        b_end = b_pre + TB;
+        b_pre = atomicAdd(g.counter, TB);
+      }
+      return b_next++;
+    }
+  };
   // ---- prologue: tickets for items 0 and 1, their structs, ticket for item 2
   unsigned long long tk = 0;  // lane 0: ticket of the item two ahead
   if (lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
+    if constexpr (MULTI) b_pre = atomicAdd(g.counter, TB);
     for (int n = 0; n < 2; ++n) {
-      const unsigned long long id = atomicAdd(g.counter, 1ull);
+      const unsigned long long id = draw();
       if (static_cast<int64_t>(id) < ntickets) {
         const Item* src = item_at(static_cast<int64_t>(id));
         cp_async16(&q_items[n], src);
@@ -151,7 +177,7 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         q_items[n].np = -1;  // end of work
       }
     }
-    tk = atomicAdd(g.counter, 1ull);
+    tk = draw();
   }
   cp_async_commit();
   cp_async_wait_all();
@@ -237,7 +263,7 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
             cp_async16(dst, src);
             cp_async16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
             if constexpr (PANELS) q_tick[(qt + 2) % QN] = static_cast<int64_t>(tk);
-            tk = atomicAdd(g.counter, 1ull);
+            tk = draw();
           } else {
             dst->np = -1;
           }
