@@ -83,6 +83,14 @@ struct RowArgs {
   // for one chunk), so C may have any number of block columns
   int64_t colw;
   int splits;     // k_row_fill CTAs per C row (long rows: chunk ranges)
+  int64_t pair_smem_off;  // k_row_fill<512>: byte offset of the pair caches
+  // warp-row fill (short rows, k_wrow_fill): pass 1 flags and lists the rows
+  // that do not fit a warp (more than 64 A entries, more than wcap_k products
+  // or wcap_d C blocks); k_row_fill_list takes those (grid-stride)
+  int32_t* wflag;                // [M] 1 = row left to the CTA fill (null: no warp fill)
+  int32_t* wlist;                // those rows
+  unsigned long long* wlist_n;   // their count
+  int wcap_k, wcap_d;
   bool dmma_ok;
   // pass 1 outputs
   int32_t* row_nnz;
@@ -124,11 +132,14 @@ __device__ __forceinline__ int band_of(int64_t j, const RowArgs& g) {
 // The symbolic kernels are instantiated for CH = 256 threads per row (long
 // rows: c1, c3, c5) and CH = 64 (short rows, many of them: c2, c4 -- four
 // times the rows in flight per SM).  CH A entries are staged per chunk
-// (= blockDim); emission windows hold kPairPT * CH pairs.
+// (= blockDim); emission windows hold pair_pt * CH pairs.
 constexpr int kChunkA = 256;   // the wide variant (host-side chunk arithmetic)
-constexpr int kPairPT = 8;     // pairs per thread in the window sort
+// pairs per thread in the window sort (4 at 512 threads: the static shared
+// memory of the sort and the pair caches stays under 48 KB)
 template <int CH>
-constexpr int pair_cap() { return kPairPT * CH; }
+constexpr int pair_pt() { return CH >= 512 ? 4 : 8; }
+template <int CH>
+constexpr int pair_cap() { return pair_pt<CH>() * CH; }
 
 template <int CH>
 struct RowChunk {  // shared-memory staging of up to CH A entries
@@ -296,13 +307,12 @@ __device__ int compact_touched(const uint32_t* bits, int nw, int32_t* tcol) {
 // Pass 1: per C block-row i -- number of C_out blocks, products, T8 slab size,
 // stored elements, per-class work items, useful flops.
 template <int CH>
-__global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
+__device__ __forceinline__ void row_count_one(const RowArgs& g, const int64_t i) {
   extern __shared__ uint32_t cnt[];
   uint32_t* bits = cnt + g.colw;
   int32_t* tcol = reinterpret_cast<int32_t*>(bits + ((g.colw + 31) >> 5));
   __shared__ unsigned long long cls_items[NSEG];
   __shared__ RowChunk<CH> rc;
-  const int64_t i = blockIdx.x;
   // empty C row (no A entries, no C_in blocks): sizes are zero, nothing else
   // (tensor-shaped operands such as c4 leave most matricized rows empty)
   if (g.a_rp[i] == g.a_rp[i + 1] && g.c_rp[i] == g.c_rp[i + 1]) {
@@ -310,6 +320,7 @@ __global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
       g.row_nnz[i] = 0;
       g.row_prod[i] = 0;
       g.row_vals[i] = 0;
+      if (g.wflag) g.wflag[i] = 0;
     }
     return;
   }
@@ -366,6 +377,11 @@ __global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
     g.row_nnz[i] = static_cast<int32_t>(t_nnz);
     g.row_prod[i] = t_prod;
     g.row_vals[i] = t_vals;
+    if (g.wflag) {  // does the row fit the warp-row fill?
+      const bool over = g.a_rp[i + 1] - g.a_rp[i] > 64 || t_prod > g.wcap_k || t_nnz > g.wcap_d;
+      g.wflag[i] = over ? 1 : 0;
+      if (over) g.wlist[atomicAdd(g.wlist_n, 1ull)] = static_cast<int32_t>(i);
+    }
     if (t_cand) atomicAdd(&g.totals[0], static_cast<unsigned long long>(t_cand));
     if (t_mnk) atomicAdd(&g.totals[1], static_cast<unsigned long long>(t_mnk) * m);
     if (t_el) atomicAdd(&g.totals[2], static_cast<unsigned long long>(t_el));
@@ -373,6 +389,12 @@ __global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
   __syncthreads();
   for (int t = threadIdx.x; t < NSEG; t += blockDim.x)
     if (cls_items[t]) atomicAdd(&g.class_items[t], cls_items[t]);
+}
+
+// one CTA per row
+template <int CH>
+__global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
+  row_count_one<CH>(g, blockIdx.x);
 }
 
 // Pass 2: emit C_out row i (columns, T8 offsets, C_in slots, per-block product
@@ -387,24 +409,35 @@ __global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
 #define BT_FILL_MINB 4
 #endif
 template <int CH>
-__global__ void __launch_bounds__(CH, BT_FILL_MINB * 256 / CH) k_row_fill(const RowArgs g) {
+__device__ __forceinline__ void row_fill_one(const RowArgs& g, const int64_t i, const int split) {
   constexpr int kPairCap = pair_cap<CH>();
+  constexpr int kPairPT = pair_pt<CH>();
   extern __shared__ uint32_t sm[];
   uint32_t* cnt = sm;                                        // counts -> C entry rank
   int32_t* cur = reinterpret_cast<int32_t*>(sm + g.colw);  // product cursor
   uint32_t* bits = sm + 2 * g.colw;                         // touched columns
   __shared__ RowChunk<CH> rc;
-  __shared__ int32_t s_bu[kPairCap];  // B tile offset of staged pair
-  __shared__ int16_t s_l[kPairCap];   // local A entry of staged pair
-  __shared__ uint32_t s_key[kPairCap];  // sorted (column, slot) keys
+  // pair caches: static for 64/256 threads; for 512 at the end of the dynamic
+  // block (g.pair_smem_off; static shared memory is capped at 48 KB)
+  constexpr int kStatCap = CH >= 512 ? 1 : kPairCap;
+  __shared__ int32_t s_bu_st[kStatCap];
+  __shared__ int16_t s_l_st[kStatCap];
+  __shared__ uint32_t s_key_st[kStatCap];
+  uint32_t* s_key = s_key_st;   // sorted (column, slot) keys
+  int32_t* s_bu = s_bu_st;      // B tile offset of staged pair
+  int16_t* s_l = s_l_st;        // local A entry of staged pair
+  if constexpr (CH >= 512) {
+    char* dyn = reinterpret_cast<char*>(sm) + g.pair_smem_off;
+    s_key = reinterpret_cast<uint32_t*>(dyn);
+    s_bu = reinterpret_cast<int32_t*>(dyn + 4 * kPairCap);
+    s_l = reinterpret_cast<int16_t*>(dyn + 8 * kPairCap);
+  }
   using Sort = cub::BlockRadixSort<uint32_t, CH, kPairPT>;
   __shared__ typename Sort::TempStorage sort_tmp;
   __shared__ unsigned long long cls_n[NSEG], cls_at[NSEG];
   // long rows: `splits` CTAs per row, CTA s emitting the products of its range
   // of A chunks (its column cursors start after the earlier ranges' pairs);
   // the row's C index and work items are written by CTA 0
-  const int64_t i = blockIdx.x / g.splits;
-  const int split = static_cast<int>(blockIdx.x % g.splits);
   if (g.out_rp[i] == g.out_rp[i + 1]) return;  // empty C row: nothing to emit
   const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
   const int nch = (a1 - a0 + CH - 1) / CH;
@@ -703,6 +736,329 @@ __global__ void __launch_bounds__(CH, BT_FILL_MINB * 256 / CH) k_row_fill(const 
   }  // split == 0
 }
 
+template <int CH>
+__global__ void __launch_bounds__(CH, BT_FILL_MINB * 256 / CH) k_row_fill(const RowArgs g) {
+  row_fill_one<CH>(g, blockIdx.x / g.splits, static_cast<int>(blockIdx.x % g.splits));
+}
+
+// list mode (rows left by the warp-row pass): one CTA per row, splits = 1
+template <int CH>
+__global__ void __launch_bounds__(CH, BT_FILL_MINB * 256 / CH) k_row_fill_list(const RowArgs g) {
+  const unsigned long long n = *g.wlist_n;
+  for (unsigned long long q = blockIdx.x; q < n; q += gridDim.x) {
+    row_fill_one<CH>(g, g.wlist[q], 0);
+    __syncthreads();
+  }
+}
+
+// ---- warp-per-row fill (short rows: c2, c4) ---------------------------------
+// One warp per C block-row, kWRows rows per CTA.  The row's distinct C columns
+// live in a per-warp open-addressing hash table in shared memory (H slots)
+// instead of the CTA fill's dense per-column arrays, whose 20 bytes per block
+// column of C bound the rows an SM holds (c2: 1 463 columns -> 29 KB per row,
+// 3 rows per SM with the pair caches; here 16-20 (H = 256) or 32+ (H = 128)
+// rows per SM, no block-wide barriers inside a row).  Same outputs as
+// k_row_fill: C columns ascending, products of a C block in ascending k (a
+// pair's rank within its column = the number of lower A entries of the row in
+// the column's 64-bit mask), so the numeric phase sees identical stacks.
+// Pass 1 (k_row_count) flags the rows that do not fit (more than 64 A
+// entries, more than 2H products, more than 3H/4 C blocks); k_row_fill_list
+// emits those.  (A warp-row count pass was measured too: slower than the CTA
+// count on c2 and c4 -- its per-row chain of pair batches is longer.)
+constexpr int kWRows = 4;  // rows (warps) per CTA: more, smaller CTAs spread c2's 1 463 rows over all SMs
+constexpr uint32_t kHEmpty = 0xffffffffu;
+
+template <int H>
+constexpr int hash_bits() { return H == 128 ? 7 : H == 256 ? 8 : 9; }
+
+// insert `col`; returns whether it is new, `slot` its slot.  The callers keep
+// the table below full occupancy (at most 3H/4 + 31 keys), so probing ends.
+template <int H>
+__device__ __forceinline__ bool hash_insert(uint32_t* hkey, uint32_t col, int& slot) {
+  uint32_t s = (col * 2654435761u) >> (32 - hash_bits<H>());
+  while (true) {
+    const uint32_t prev = atomicCAS(&hkey[s], kHEmpty, col);
+    if (prev == kHEmpty || prev == col) {
+      slot = static_cast<int>(s);
+      return prev == kHEmpty;
+    }
+    s = (s + 1) & (H - 1);
+  }
+}
+
+// last A entry (lane) l < nac of the chunk with ex_l <= t (ex = exclusive
+// prefix of the B-row lengths, one per lane)
+__device__ __forceinline__ int warp_find_entry(int32_t ex, int nac, int32_t t) {
+  int l = 0;
+#pragma unroll
+  for (int st = 16; st; st >>= 1) {
+    const int c = l + st;
+    const int32_t v = __shfl_sync(0xffffffffu, ex, c & 31);
+    if (c < nac && v <= t) l = c;
+  }
+  return l;
+}
+
+// Per-warp shared memory of the fill pass (bytes): hmask u64[H], hkey u32[H],
+// hcnt u32[H], pinfo u32[2H], pbu i32[2H], dl / ord / nbuf u32[3H/4] each,
+// A-entry tables 3 x i32[64]
+template <int H>
+__host__ __device__ constexpr size_t wrow_fill_bytes() {
+  return static_cast<size_t>(41 * H + 768);
+}
+
+// Candidate pairs are taken in groups of kWU x 32: every lane computes its kWU
+// pairs' B entries and issues all their loads (norms, B column, B offset)
+// before any hash work, so a group costs one memory round trip instead of kWU
+// (the per-row chain of dependent DRAM round trips is what bounds these
+// latency-bound passes).
+constexpr int kWU = 4;
+
+template <int H>
+__global__ void __launch_bounds__(kWRows * 32) k_wrow_fill(const RowArgs g, const int64_t M) {
+  constexpr int DMAX = 3 * H / 4, NR = (DMAX + 31) / 32;
+  extern __shared__ __align__(16) unsigned char wfm[];
+  __shared__ unsigned long long cls_n[NSEG], cls_at[NSEG];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned char* base = wfm + w * wrow_fill_bytes<H>();
+  unsigned long long* hmask = reinterpret_cast<unsigned long long*>(base);
+  uint32_t* hkey = reinterpret_cast<uint32_t*>(base + 8 * H);   // column, then product cursor
+  uint32_t* hcnt = reinterpret_cast<uint32_t*>(base + 12 * H);  // products | (C_in index + 1) << 8
+  uint32_t* pinfo = reinterpret_cast<uint32_t*>(base + 16 * H); // kept pair: slot << 8 | A entry
+  int32_t* pbu = reinterpret_cast<int32_t*>(base + 24 * H);     // kept pair: B tile offset
+  uint32_t* dl = reinterpret_cast<uint32_t*>(base + 32 * H);    // distinct keys, then item offsets
+  uint32_t* ord = dl + DMAX;                                    // keys by ascending column
+  int32_t* nbuf = reinterpret_cast<int32_t*>(ord + DMAX);       // n of ord[r]
+  int32_t* a_au = reinterpret_cast<int32_t*>(base + 41 * H);    // per A entry of the row
+  int32_t* a_k = a_au + 64;
+  int32_t* a_kc = a_k + 64;
+  for (int t = threadIdx.x; t < NSEG; t += blockDim.x) cls_n[t] = 0;
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * kWRows + w;
+  const bool act = i < M && !g.wflag[i] && g.out_rp[i] != g.out_rp[i + 1];
+  int D = 0, m = 0;
+  int32_t ci0 = 0;
+  int64_t pbase = 0, vbase = 0;
+  if (act) {
+    const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
+    ci0 = g.c_rp[i];
+    const int32_t ci1 = g.c_rp[i + 1];
+    m = g.m_sz[i];
+    const int32_t cbase = g.out_rp[i];
+    pbase = g.prod_base[i];
+    vbase = g.val_base[i];
+    for (int s = lane; s < H; s += 32) {
+      hkey[s] = kHEmpty;
+      hcnt[s] = 0u;
+      hmask[s] = 0ull;
+    }
+    __syncwarp();
+    for (int32_t e = ci0 + lane; e < ci1; e += 32) {  // C_in blocks (distinct columns)
+      int s;
+      hash_insert<H>(hkey, static_cast<uint32_t>(g.c_col[e]), s);
+      hcnt[s] = static_cast<uint32_t>(e - ci0 + 1) << 8;
+    }
+    __syncwarp();
+    int K = 0;
+    for (int32_t cb = a0; cb < a1; cb += 32) {
+      const int32_t e = cb + lane;
+      const int nac = min(32, a1 - cb);
+      int32_t b0 = 0, len = 0;
+      if (e < a1) {
+        const int32_t k = g.a_col[e];
+        b0 = g.b_rp[k];
+        len = g.b_rp[k + 1] - b0;
+        const int lr = cb - a0 + lane;
+        a_k[lr] = k;
+        a_kc[lr] = (g.k_sz[k] + 3) >> 2;
+        a_au[lr] = static_cast<int32_t>(g.a_off[e] >> 6);
+      }
+      int32_t incl = len;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const int32_t ex = incl - len;
+      const int32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      for (int32_t t0 = 0; t0 < tot; t0 += kWU * 32) {
+        int32_t colv[kWU], buv[kWU];
+        int lrv[kWU];
+        bool keepv[kWU];
+#pragma unroll
+        for (int u = 0; u < kWU; ++u) {  // all loads of the group first
+          const int32_t t = t0 + u * 32 + lane;
+          const bool valid = t < tot;
+          const int l = warp_find_entry(ex, nac, t);
+          const int32_t f = __shfl_sync(0xffffffffu, b0, l) + t - __shfl_sync(0xffffffffu, ex, l);
+          lrv[u] = cb - a0 + l;
+          keepv[u] = valid && keep_product(g.na, g.nb, cb + l, f, g.eps);
+          colv[u] = valid ? g.b_col[f] : 0;
+          buv[u] = valid ? static_cast<int32_t>(g.b_off[f] >> 6) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kWU; ++u) {
+          int s = 0;
+          if (keepv[u]) {
+            hash_insert<H>(hkey, static_cast<uint32_t>(colv[u]), s);
+            atomicAdd(&hcnt[s], 1u);
+            atomicOr(&hmask[s], 1ull << lrv[u]);
+          }
+          const unsigned kb = __ballot_sync(0xffffffffu, keepv[u]);
+          if (keepv[u]) {
+            const int kp = K + __popc(kb & lt);
+            pinfo[kp] = (static_cast<uint32_t>(s) << 8) | static_cast<uint32_t>(lrv[u]);
+            pbu[kp] = buv[u];
+          }
+          K += __popc(kb);
+        }
+      }
+    }
+    __syncwarp();
+    // distinct columns -> dl (slot order), then ranked by column into ord
+    for (int s0 = 0; s0 < H; s0 += 32) {
+      const int s = s0 + lane;
+      const uint32_t col = hkey[s];
+      const bool occ = col != kHEmpty;
+      const unsigned b = __ballot_sync(0xffffffffu, occ);
+      if (occ) dl[D + __popc(b & lt)] = (col << 9) | static_cast<uint32_t>(s);
+      D += __popc(b);
+    }
+    BT_DASSERT(D <= DMAX, "warp-row distinct columns");
+    // rank of each key = number of smaller keys (keys are distinct), four per
+    // 16-byte shared load (the list is padded with keys above every real one)
+    const int D4 = (D + 3) & ~3;
+    if (lane < D4 - D) dl[D + lane] = 0xffffffffu;
+    __syncwarp();
+    for (int d = lane; d < D; d += 32) {
+      const uint32_t key = dl[d];
+      int r = 0;
+      const uint4* dl4 = reinterpret_cast<const uint4*>(dl);
+      for (int x = 0; x < D4 / 4; ++x) {
+        const uint4 v = dl4[x];
+        r += (v.x < key) + (v.y < key) + (v.z < key) + (v.w < key);
+      }
+      ord[r] = key;
+    }
+    __syncwarp();
+    {
+      int nr[NR];  // column sizes of the C entries, all loads in flight
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int r = q * 32 + lane;
+        nr[q] = r < D ? g.n_sz[ord[r] >> 9] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < NR; ++q)
+        if (q * 32 + lane < D) nbuf[q * 32 + lane] = nr[q];
+    }
+    __syncwarp();
+    // C entries in column order: C index, slab offsets, product ranges; the
+    // column's product cursor replaces its key in hkey, the entry's offset
+    // within its work-item segment goes to dl
+    long long run_p = 0, run_v = 0;
+    for (int r0 = 0; r0 < D; r0 += 32) {
+      const int r = r0 + lane;
+      const bool ok = r < D;
+      const uint32_t key = ok ? ord[r] : 0u;
+      const int32_t col = static_cast<int32_t>(key >> 9);
+      const int s = static_cast<int>(key & 511u);
+      const uint32_t hc = ok ? hcnt[s] : 0u;
+      const int np = static_cast<int>(hc & 0xffu);
+      const int cin_l = static_cast<int>(hc >> 8) - 1;
+      const int n = ok ? nbuf[r] : 0;
+      const long long tv = ok ? t8_size(m, n) : 0;
+      long long pi = np, vi = tv;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const long long py = __shfl_up_sync(0xffffffffu, pi, d);
+        const long long vy = __shfl_up_sync(0xffffffffu, vi, d);
+        if (lane >= d) {
+          pi += py;
+          vi += vy;
+        }
+      }
+      if (ok) {
+        const int32_t c = cbase + r;
+        const long long p_ex = run_p + pi - np;
+        g.out_col[c] = col;
+        g.out_row[c] = static_cast<int32_t>(i);
+        g.out_off[c] = vbase + run_v + vi - tv;
+        g.cin_map[c] = cin_l >= 0 ? g.c_off[ci0 + cin_l] : -1;
+        g.out_np[c] = np;
+        g.out_p0[c] = pbase + p_ex;
+        hkey[s] = static_cast<uint32_t>(p_ex);
+        const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
+        const int seg = cls * kMaxBands + band_of(col, g);
+        dl[r] = static_cast<uint32_t>(
+            agg_add(&cls_n[seg], seg, static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows))));
+      }
+      run_p += __shfl_sync(0xffffffffu, pi, 31);
+      run_v += __shfl_sync(0xffffffffu, vi, 31);
+    }
+    __syncwarp();
+    // product descriptors: slot = column cursor + rank of the A entry among
+    // the column's entries (k ascending)
+    for (int kp = lane; kp < K; kp += 32) {
+      const uint32_t info = pinfo[kp];
+      const int s = static_cast<int>(info >> 8), lr = static_cast<int>(info & 0xffu);
+      const int32_t p = static_cast<int32_t>(hkey[s]) + __popcll(hmask[s] & ((1ull << lr) - 1ull));
+      BT_DASSERT(p >= 0 && pbase + p < g.prod_base[i + 1], "warp-row descriptor slot");
+      g.desc[pbase + p] = make_int4(a_au[lr], pbu[kp], a_kc[lr], a_k[lr]);
+    }
+  }
+  __syncthreads();
+  // one reservation per (class, band) segment for the CTA's rows
+  for (int t = threadIdx.x; t < NSEG; t += blockDim.x) {
+    const unsigned long long k = cls_n[t];
+    cls_at[t] = k ? atomicAdd(&g.class_cursor[t], k) : 0ull;
+  }
+  __syncthreads();
+  if (!act) return;
+  // work items (tall blocks become tall_rows-row tiles)
+  long long run_v = 0;
+  for (int r0 = 0; r0 < D; r0 += 32) {
+    const int r = r0 + lane;
+    const bool ok = r < D;
+    const uint32_t key = ok ? ord[r] : 0u;
+    const int32_t col = static_cast<int32_t>(key >> 9);
+    const int s = static_cast<int>(key & 511u);
+    const int n = ok ? nbuf[r] : 0;
+    const long long tv = ok ? t8_size(m, n) : 0;
+    long long vi = tv;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const long long vy = __shfl_up_sync(0xffffffffu, vi, d);
+      if (lane >= d) vi += vy;
+    }
+    if (ok) {
+      const uint32_t hc = hcnt[s];
+      const int cin_l = static_cast<int>(hc >> 8) - 1;
+      const int64_t c_off = vbase + run_v + vi - tv;
+      const int64_t cin = cin_l >= 0 ? g.c_off[ci0 + cin_l] : -1;
+      const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
+      const int nt = class_tiles(m, cls, g.tall_rows);
+      const int seg = cls * kMaxBands + band_of(col, g);
+      const unsigned long long at = cls_at[seg] + dl[r];
+      const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
+      for (int q = 0; q < nt; ++q) {
+        const int rt = g.tall_rows * q;
+        Item it;
+        it.c_off = c_off + (rt >> 3) * tile_row;
+        it.cin_off = cin >= 0 ? cin + (rt >> 3) * tile_row : -1;
+        it.p0r8 = (pbase + static_cast<int64_t>(hkey[s])) | (static_cast<int64_t>(rt >> 3) << 48);
+        it.np = static_cast<int32_t>(hc & 0xffu);
+        it.rows = static_cast<int16_t>(nt > 1 ? min(g.tall_rows, m - rt) : m);
+        it.n = static_cast<int16_t>(n);
+        BT_DASSERT(static_cast<int64_t>(at) + q < g.nitems_total, "warp-row work item slot");
+        g.items[at + q] = it;
+      }
+    }
+    run_v += __shfl_sync(0xffffffffu, vi, 31);
+  }
+}
+
 // K-panel work items (L2 blocking of long product chains):
 // item t of panel p covers the products of base item t whose k block lies in
 // [kb[p], kb[p+1]) -- a sub-range, products being in ascending k.  Panel 0
@@ -765,8 +1121,6 @@ __device__ void init_cursors(const unsigned long long* __restrict__ seg_items,
   for (int q = threadIdx.x; q < NCLASS; q += blockDim.x) cursor[NSEG + q] = 0ull;
 }
 
-// Exclusive scans of the three per-row arrays in one single-CTA kernel (small M);
-// element M receives the totals.
 // Exclusive scans of the three per-row arrays in one single-CTA kernel (M <=
 // 8192 rows); element M receives the totals.  Thread t owns the PER
 // consecutive rows [t*PER, t*PER + PER): it sums them, the three sums are
@@ -1090,13 +1444,38 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     // nothing, profiles/r02/row_threads_ab.txt)
     int row_threads = (a_per_row <= 48.0 && a_per_row * b_per_row <= 384.0 &&
                        M >= 2 * x.num_sms && row_smem <= 12 * 1024) ? 64 : 256;
-    row_threads = env_int("BT_ROW_THREADS", row_threads) == 64 ? 64 : 256;
+    {
+      const int rt = env_int("BT_ROW_THREADS", row_threads);
+      row_threads = rt == 64 ? 64 : rt == 512 ? 512 : 256;
+    }
     if (row_threads == 64) fill_splits = 1;
+    // warp-per-row fill for short rows (one warp per C row, a hash of the
+    // row's columns instead of dense per-column arrays): H = 128 for ~<= 48
+    // candidate pairs per row (c4), 256 up to ~120 (or ~240 with an eps
+    // filter, which keeps a fraction of them: c2); pass 1 lists the rows that
+    // do not fit for the CTA fill (BT_WARP_ROWS=0/128/256 overrides)
+    int wrow_h = 0;
+    {
+      const double pairs = a_per_row * b_per_row;
+      if (N < (int64_t(1) << 23) && a_per_row <= 24.0 && M >= x.num_sms) {
+        if (pairs <= 48.0) wrow_h = 128;
+        else if (pairs <= (eps > 0 ? 240.0 : 120.0)) wrow_h = 256;
+      }
+      const int e = env_int("BT_WARP_ROWS", -1);
+      if (e == 0 || e == 128 || e == 256) wrow_h = e;
+      if (N >= (int64_t(1) << 23)) wrow_h = 0;
+    }
+    if (wrow_h) fill_splits = 1;  // (the list fill takes one CTA per left-over row)
     BT_REQUIRE(row_smem <= 180 * 1024, BT_ERR_INTERNAL, "multiply: column chunk too wide");
     // split CTAs need 4 more bytes per column; if that does not fit, one CTA
     // per row
     if (fill_splits > 1 && row_smem + 4 * static_cast<size_t>(W) > 180 * 1024) fill_splits = 1;
     if (fill_splits > 1) row_smem += 4 * static_cast<size_t>(W);
+    size_t pair_off = 0;
+    if (row_threads == 512) {  // the 512-thread fill keeps its pair caches here
+      pair_off = (row_smem + 15) & ~size_t(15);
+      row_smem = pair_off + 10 * static_cast<size_t>(pair_cap<512>());
+    }
 
     // ---- norms for the eps filter, cached with the stores: a
     // store's norms are computed once after it changes (both in one launch
@@ -1145,6 +1524,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.tall_rows = env_int("BT_TALL_ROWS", 32) == 24 ? 24 : 32;
     ra.tiny = env_int("BT_DFMA", 1) != 0;
     ra.splits = fill_splits;
+    ra.pair_smem_off = static_cast<int64_t>(pair_off);
     ra.colw = colw;
     {
       // column bands: when A and B together overflow a comfortable share of L2
@@ -1167,8 +1547,11 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     int64_t* row_vals = x.ws<int64_t>(2, M + 1);
     int64_t* prod_base = x.ws<int64_t>(3, M + 1);
     int64_t* val_base = x.ws<int64_t>(4, M + 1);
-    unsigned long long* tot = x.ws<unsigned long long>(5, 3 + NSEG);
-    BT_CUDA(cudaMemsetAsync(tot, 0, sizeof(unsigned long long) * (3 + NSEG), st));
+    // [0..3) totals, [3, 3 + NSEG) work items per segment, [3 + NSEG] rows
+    // the warp-row pass left to the CTA kernels
+    constexpr int kTot = 4 + NSEG;
+    unsigned long long* tot = x.ws<unsigned long long>(5, kTot);
+    BT_CUDA(cudaMemsetAsync(tot, 0, sizeof(unsigned long long) * kTot, st));
     // sizes for the host: written by the scan kernel straight into mapped
     // page-locked memory (a copy-engine D2H would queue behind an
     // asynchronous export's transfer)
@@ -1186,10 +1569,17 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.row_vals = row_vals;
     ra.totals = tot;
     ra.class_items = tot + 3;
+    ra.wflag = wrow_h ? x.ws<int32_t>(11, M) : nullptr;
+    ra.wlist = x.ws<int32_t>(12, M);
+    ra.wlist_n = tot + 3 + NSEG;
+    ra.wcap_k = 2 * wrow_h;
+    ra.wcap_d = 3 * wrow_h / 4;
+    const size_t sm1 = static_cast<size_t>(W) * 8 + 4 * ((W + 31) / 32);
     if (M > 0) {
-      const size_t sm1 = static_cast<size_t>(W) * 8 + 4 * ((W + 31) / 32);
       // static + dynamic shared memory may exceed the 48 KB default: always opt in
-      auto count_fn = row_threads == 64 ? k_row_count<64> : k_row_count<256>;
+      auto count_fn = row_threads == 64    ? k_row_count<64>
+                      : row_threads == 512 ? k_row_count<512>
+                                           : k_row_count<256>;
       ensure_dyn_smem(reinterpret_cast<const void*>(count_fn), sm1);
       count_fn<<<static_cast<unsigned>(M), row_threads, sm1, st>>>(ra);
       check_launch("row_count");
@@ -1197,7 +1587,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     }
     if (M <= 8192) {
       k_scan_rows<<<1, 1024, 0, st>>>(row_nnz, row_prod, row_vals, M, out_rp.p, prod_base,
-                                      val_base, tot, 3 + NSEG, dsizes, cursor, ready_dev, seq);
+                                      val_base, tot, kTot, dsizes, cursor, ready_dev, seq);
       check_launch("scan_rows");
       count_launch(&x);
     } else {
@@ -1207,14 +1597,14 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       exclusive_scan(x, row_nnz, out_rp.p, M + 1);
       exclusive_scan(x, row_prod, prod_base, M + 1);
       exclusive_scan(x, row_vals, val_base, M + 1);
-      k_pack_sizes<<<1, 256, 0, st>>>(out_rp.p, prod_base, val_base, M, tot, 3 + NSEG, dsizes,
+      k_pack_sizes<<<1, 256, 0, st>>>(out_rp.p, prod_base, val_base, M, tot, kTot, dsizes,
                                       cursor, ready_dev, seq);
       check_launch("pack_sizes");
       count_launch(&x);
     }
     struct Sizes {
       unsigned long long nout, nprod, nvals;
-      unsigned long long tot[3 + NSEG];
+      unsigned long long tot[kTot];
     };
     static_assert(sizeof(Sizes) <= 2048, "pinned staging");
     // the scan kernel wrote the sizes into mapped pinned memory (no D2H copy)
@@ -1292,8 +1682,30 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.nprod_total = nprod;
     ra.nitems_total = nitems;
     if (phases) BT_CUDA(cudaEventRecord(x.ev[5], st));
-    if (nout > 0) {
-      auto fill_fn = row_threads == 64 ? k_row_fill<64> : k_row_fill<256>;
+    const int64_t nleft = wrow_h ? static_cast<int64_t>(h.tot[3 + NSEG]) : 0;
+    if (env_int("BT_TRACE", 0) && wrow_h)
+      fprintf(stderr, "[bt] warp-row fill (H=%d): %lld of %lld rows left to the CTA fill\n",
+              wrow_h, static_cast<long long>(nleft), static_cast<long long>(M));
+    if (nout > 0 && wrow_h) {
+      const unsigned grid = static_cast<unsigned>((M + kWRows - 1) / kWRows);
+      const size_t smw = static_cast<size_t>(kWRows) *
+                         (wrow_h == 128 ? wrow_fill_bytes<128>() : wrow_fill_bytes<256>());
+      auto wfn = wrow_h == 128 ? k_wrow_fill<128> : k_wrow_fill<256>;
+      ensure_dyn_smem(reinterpret_cast<const void*>(wfn), smw);
+      wfn<<<grid, kWRows * 32, smw, st>>>(ra, M);
+      check_launch("wrow_fill");
+      count_launch(&x);
+      if (nleft > 0) {
+        ensure_dyn_smem(reinterpret_cast<const void*>(k_row_fill_list<256>), row_smem);
+        k_row_fill_list<256><<<static_cast<unsigned>(std::min<int64_t>(nleft, 4 * x.num_sms)), 256, row_smem,
+                          st>>>(ra);
+        check_launch("row_fill_list");
+        count_launch(&x);
+      }
+    } else if (nout > 0) {
+      auto fill_fn = row_threads == 64    ? k_row_fill<64>
+                     : row_threads == 512 ? k_row_fill<512>
+                                          : k_row_fill<256>;
       ensure_dyn_smem(reinterpret_cast<const void*>(fill_fn), row_smem);
       fill_fn<<<static_cast<unsigned>(M * fill_splits), row_threads, row_smem, st>>>(ra);
       check_launch("row_fill");

@@ -511,3 +511,47 @@ def test_random_sweep(oracle, ctx, seed):
     assert st["products"] == nprod
     assert st["flops"] == flops
     assert_parity(from_store(c), want)
+
+
+@pytest.mark.parametrize("h", ["128", "256"])
+@pytest.mark.parametrize("seed", range(9))
+def test_warp_row_symbolic(oracle, ctx, monkeypatch, h, seed):
+    """The warp-per-row fill (BT_WARP_ROWS=128/256: one warp per C row, a hash
+    of the row's columns) against the oracle and bit-identical to the CTA
+    fill (BT_WARP_ROWS=0): random shapes and block-size palettes (tiny DFMA,
+    DMMA classes, tall rows, generic n > 32), C_in, the eps filter, empty
+    rows.  Seeds 0, 3, 6 also hold rows too long for a warp (more than 64 A
+    entries, more C blocks or products than the hash takes), which pass 1
+    lists for the CTA fill (k_row_fill_list)."""
+    from paper_1910_13555_b200.store import multiply_local
+    rng = np.random.default_rng(7100 + seed)
+    pal = lambda: rng.choice(np.arange(1, 41), size=int(rng.integers(1, 4)), replace=False)
+    pm = pal()
+    if seed % 4 == 1:
+        pm = np.append(pm, 169)                  # tall rows
+    nm, nk, nn = int(rng.integers(150, 400)), int(rng.integers(20, 200)), int(rng.integers(20, 500))
+    rsz = rng.choice(pm, nm).astype(np.int32)
+    ksz = rng.choice(pal(), nk).astype(np.int32)
+    pn = pal()
+    if seed % 4 == 2:
+        pn = np.append(pn, 48)                   # generic (n > 32)
+    nsz = rng.choice(pn, nn).astype(np.int32)
+    scale = 6.0 if seed % 2 else 0.0
+    A = oracle.random_matrix(7200 + seed, rsz, ksz, float(rng.choice([0.01, 0.03, 0.08])), scale)
+    if seed % 3 == 0:                            # a few long rows
+        A = _dense_rows(oracle, A, rsz, ksz, rng)
+    B = oracle.random_matrix(7300 + seed, ksz, nsz, float(rng.choice([0.02, 0.05, 0.1])), scale)
+    Cin = oracle.random_matrix(7400 + seed, rsz, nsz, 0.05 * float(seed % 2 == 0), scale)
+    eps = 1e-3 if scale else 0.0
+    want, nprod, flops = oracle.multiply(A, B, Cin, eps)
+    out = {}
+    for mode in ("0", h):
+        monkeypatch.setenv("BT_WARP_ROWS", mode)
+        a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+        st = multiply_local(ctx, a, b, c, eps)
+        assert st["products"] == nprod and st["flops"] == flops
+        got = from_store(c)
+        assert_parity(got, want)
+        out[mode] = got
+    assert np.array_equal(out["0"].bi, out[h].bi) and np.array_equal(out["0"].bj, out[h].bj)
+    assert np.array_equal(out["0"].vals, out[h].vals)
