@@ -1522,7 +1522,15 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.sort_min = env_int("BT_SORT_MIN", 48);
     ra.colmask = colmask;
     ra.tall_rows = env_int("BT_TALL_ROWS", 32) == 24 ? 24 : 32;
-    ra.tiny = env_int("BT_DFMA", 1) != 0;
+    // tiny C blocks (m, n <= 5) go to the DFMA kernel when every C block is
+    // tiny; in a mixed basis they ride along in the MULTI DMMA launch, which
+    // (with batched tickets) beats the DFMA kernel beside it: c2 numeric
+    // 108 -> 102 us (the DFMA grid only gets SMs in the MULTI tail, and
+    // launched first it slows the sweep to 145 us).  BT_DFMA=0/1 forces.
+    {
+      const bool all_tiny = Cm.max_r <= kTinyMax && Cm.max_c <= kTinyMax;
+      ra.tiny = env_int("BT_DFMA", all_tiny ? 1 : 0) != 0;
+    }
     ra.splits = fill_splits;
     ra.pair_smem_off = static_cast<int64_t>(pair_off);
     ra.colw = colw;
