@@ -84,6 +84,11 @@ struct RowArgs {
   int64_t colw;
   int splits;     // k_row_fill CTAs per C row (long rows: chunk ranges)
   int64_t pair_smem_off;  // k_row_fill<512>: byte offset of the pair caches
+  // split-count mode (few long rows): [M][splits + 1][ncols] column counts of
+  // each CTA's range of A chunks (k_row_count_split), turned by pass 1 into
+  // the kept pairs of the earlier ranges (slot s) and the row total (slot
+  // splits), so the fill CTAs of a row need not recount it; null otherwise
+  int32_t* snap;
   // warp-row fill (short rows, k_wrow_fill): pass 1 flags and lists the rows
   // that do not fit a warp (more than 64 A entries, more than wcap_k products
   // or wcap_d C blocks); k_row_fill_list takes those (grid-stride)
@@ -266,6 +271,46 @@ __device__ bool row_products(const RowArgs& g, int64_t i, uint32_t* cnt, uint32_
   return cached;
 }
 
+// Split-count mode: the column counts of row i from pass 1's snapshots
+// (DESIGN.md 4.2).  finalize (pass 1): sums the per-range counts, leaves the
+// exclusive prefix per range in slot s and the total in slot S; fill: reads
+// the total and, for range `split` > 0, the earlier ranges' pairs (`before`).
+// Then the touched bits and the C_in flags as row_products sets them.
+__device__ __forceinline__ void snap_counts(const RowArgs& g, int64_t i, uint32_t* cnt,
+                                            uint32_t* bits, uint32_t* before, int split,
+                                            bool finalize) {
+  const int S = g.splits;
+  const int64_t N = g.ncols;
+  int32_t* row = g.snap + i * (S + 1) * N;
+  for (int w = threadIdx.x; w < static_cast<int>((N + 31) >> 5); w += blockDim.x) bits[w] = 0u;
+  for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
+    uint32_t tot;
+    if (finalize) {
+      int32_t run = 0;
+      for (int s = 0; s < S; ++s) {
+        const int32_t v = row[s * N + j];
+        row[s * N + j] = run;
+        run += v;
+      }
+      row[S * N + j] = run;
+      tot = static_cast<uint32_t>(run);
+    } else {
+      tot = static_cast<uint32_t>(row[S * N + j]);
+      if (before) before[j] = static_cast<uint32_t>(row[split * N + j]);
+    }
+    cnt[j] = tot;
+  }
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < N; j += blockDim.x)
+    if (cnt[j]) atomicOr(&bits[j >> 5], 1u << (j & 31));
+  for (int32_t e = g.c_rp[i] + threadIdx.x; e < g.c_rp[i + 1]; e += blockDim.x) {
+    const int64_t j = g.c_col[e];
+    cnt[j] |= kCinFlag;
+    atomicOr(&bits[j >> 5], 1u << (j & 31));
+  }
+  __syncthreads();
+}
+
 // Warp-aggregated shared-memory atomicAdd: lanes adding to the same counter
 // (same class) are combined, one atomic per group; returns each lane's slot.
 __device__ __forceinline__ unsigned long long agg_add(unsigned long long* ctr, int key,
@@ -331,7 +376,10 @@ __device__ __forceinline__ void row_count_one(const RowArgs& g, const int64_t i)
   // column chunks (one when the row fits the shared-memory counters)
   for (int64_t j0 = 0; j0 < g.ncols; j0 += g.colw) {
     const int64_t jw = min(g.colw, g.ncols - j0);
-    row_products(g, i, cnt, bits, rc, &cand, &mnk, j0, jw);
+    if (g.snap)  // (candidates and flops were added by k_row_count_split)
+      snap_counts(g, i, cnt, bits, nullptr, 0, true);
+    else
+      row_products(g, i, cnt, bits, rc, &cand, &mnk, j0, jw);
     const int ntouch = compact_touched<CH>(bits, static_cast<int>((jw + 31) >> 5), tcol);
     for (int q = threadIdx.x; q < ntouch; q += blockDim.x) {
       const int jl = tcol[q];
@@ -395,6 +443,54 @@ __device__ __forceinline__ void row_count_one(const RowArgs& g, const int64_t i)
 template <int CH>
 __global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
   row_count_one<CH>(g, blockIdx.x);
+}
+
+// Split-count mode, first step: CTA (i, s) counts the kept pairs of its range
+// of A chunks per C column (the fill's ranges) into snap[i][s][:], and adds
+// its candidates and useful flops to the totals.  k_row_count then sums the
+// ranges per row (snap_counts).  c3's 100 rows of ~2 000 A entries: one CTA
+// per row left most SMs idle and every fill CTA recounted its whole row.
+template <int CH>
+__global__ void __launch_bounds__(CH) k_row_count_split(const RowArgs g) {
+  extern __shared__ uint32_t cnt[];  // [ncols]
+  __shared__ RowChunk<CH> rc;
+  const int S = g.splits;
+  const int64_t i = blockIdx.x / S;
+  const int split = static_cast<int>(blockIdx.x % S);
+  const int64_t N = g.ncols;
+  const int32_t a0 = g.a_rp[i], a1 = g.a_rp[i + 1];
+  for (int64_t j = threadIdx.x; j < N; j += CH) cnt[j] = 0u;
+  __syncthreads();
+  const int nch = (a1 - a0 + CH - 1) / CH;
+  const int ch_lo = static_cast<int>((static_cast<int64_t>(split) * nch) / S);
+  const int ch_hi = static_cast<int>((static_cast<int64_t>(split + 1) * nch) / S);
+  unsigned long long cand = 0, mnk = 0;
+  for (int ch = ch_lo; ch < ch_hi; ++ch) {
+    const int32_t c0 = a0 + ch * CH;
+    const int n = min(CH, a1 - c0);
+    const int64_t T = stage_chunk<CH>(g, c0, a1, rc, 0, N);
+    for (int64_t t = threadIdx.x; t < T; t += CH) {
+      const int l = find_entry(rc, n, static_cast<int32_t>(t));
+      const int32_t f = rc.b0[l] + static_cast<int32_t>(t - rc.pref[l]);
+      ++cand;
+      if (!keep_product(g.na, g.nb, c0 + l, f, g.eps)) continue;
+      const int32_t j = g.b_col[f];
+      atomicAdd(&cnt[j], 1u);
+      mnk += static_cast<unsigned long long>(rc.ksz[l]) * g.n_sz[j];
+    }
+    __syncthreads();
+  }
+  int32_t* out = g.snap + (i * (S + 1) + split) * N;
+  for (int64_t j = threadIdx.x; j < N; j += CH) out[j] = static_cast<int32_t>(cnt[j]);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    cand += __shfl_xor_sync(0xffffffffu, cand, d);
+    mnk += __shfl_xor_sync(0xffffffffu, mnk, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (cand) atomicAdd(&g.totals[0], cand);
+    if (mnk) atomicAdd(&g.totals[1], mnk * static_cast<unsigned long long>(g.m_sz[i]));
+  }
 }
 
 // Pass 2: emit C_out row i (columns, T8 offsets, C_in slots, per-block product
@@ -463,8 +559,12 @@ __device__ __forceinline__ void row_fill_one(const RowArgs& g, const int64_t i, 
   for (int64_t j0 = 0; j0 < g.ncols; j0 += g.colw) {
   const int64_t jw = min(g.colw, g.ncols - j0);
   // single-chunk rows: pair columns / B offsets cached, rc stays staged
-  const bool cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, j0, jw, s_key, s_bu,
-                                   s_l, before, e_lo);
+  bool cached = false;
+  if (g.snap)  // split-count mode: counts (and the earlier ranges') from pass 1
+    snap_counts(g, i, cnt, bits, before, split, false);
+  else
+    cached = row_products(g, i, cnt, bits, rc, nullptr, nullptr, j0, jw, s_key, s_bu, s_l, before,
+                          e_lo);
   const int ntouch = compact_touched<CH>(bits, static_cast<int>((jw + 31) >> 5), tcol);
   {
     // touched columns in ascending order, 256 at a time: ranks, product bases
@@ -658,9 +758,23 @@ __device__ __forceinline__ void row_fill_one(const RowArgs& g, const int64_t i, 
           }
         }
       }
-      Sort(sort_tmp).Sort(keys);  // blocked arrangement: thread owns ranks [tid*PT, ...)
+      // blocked arrangement: thread owns ranks [tid*PT, ...); only the live
+      // key bits are sorted (11 slot bits + the chunk's column bits; the
+      // filtered-out key's low bits are all ones, above every real key)
+      Sort(sort_tmp).Sort(keys, 0, 11 + (32 - __clz(static_cast<int>(jw))));
 #pragma unroll
       for (int u = 0; u < kPairPT; ++u) s_key[threadIdx.x * kPairPT + u] = keys[u];
+      __syncthreads();
+      // run heads: the first rank of each column's run in this window goes to
+      // run0[column] (cnt is free here: the C entry ranks were used above)
+      uint32_t* run0 = cnt;
+#pragma unroll
+      for (int u = 0; u < kPairPT; ++u) {
+        const uint32_t key = keys[u];
+        const int q = threadIdx.x * kPairPT + u;
+        if (key != 0xffffffffu && (q == 0 || (s_key[q - 1] >> 11) != (key >> 11)))
+          run0[key >> 11] = static_cast<uint32_t>(q);
+      }
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < kPairPT; ++u) {
@@ -668,12 +782,7 @@ __device__ __forceinline__ void row_fill_one(const RowArgs& g, const int64_t i, 
         if (key == 0xffffffffu) continue;
         const int q = threadIdx.x * kPairPT + u;
         const uint32_t jkey = key >> 11;
-        // first rank of this column's run
-        int lo = 0, hi = q;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if ((s_key[mid] >> 11) < jkey) lo = mid + 1; else hi = mid;
-        }
+        const int lo = static_cast<int>(run0[jkey]);  // first rank of this column's run
         const int slot = static_cast<int>(key & 0x7ffu);
         const int l = s_l[slot];
         const int kc = (rc.ksz[l] + 3) >> 2;
@@ -689,14 +798,7 @@ __device__ __forceinline__ void row_fill_one(const RowArgs& g, const int64_t i, 
         const uint32_t key = s_key[q];
         if (key == 0xffffffffu) continue;
         const bool run_end = q + 1 == kPairCap || (s_key[q + 1] >> 11) != (key >> 11);
-        if (run_end) {
-          int lo = 0, hi = q;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((s_key[mid] >> 11) < (key >> 11)) lo = mid + 1; else hi = mid;
-          }
-          cur[key >> 11] += q - lo + 1;
-        }
+        if (run_end) cur[key >> 11] += q - static_cast<int>(run0[key >> 11]) + 1;
       }
       __syncthreads();
     }
@@ -1471,6 +1573,12 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     // per row
     if (fill_splits > 1 && row_smem + 4 * static_cast<size_t>(W) > 180 * 1024) fill_splits = 1;
     if (fill_splits > 1) row_smem += 4 * static_cast<size_t>(W);
+    // split-count mode (few long rows, one column chunk): pass 1 counts each
+    // fill CTA's range of A chunks in its own CTA and keeps the per-range
+    // column counts, so the fill CTAs of a row do not recount the row
+    const bool snap_mode = fill_splits > 1 && N <= colw && env_int("BT_SNAP", 1) != 0 &&
+                           static_cast<double>(M) * (fill_splits + 1) * static_cast<double>(N) * 4.0 <= 64e6;
+    if (snap_mode) row_threads = 256;
     size_t pair_off = 0;
     if (row_threads == 512) {  // the 512-thread fill keeps its pair caches here
       pair_off = (row_smem + 15) & ~size_t(15);
@@ -1533,6 +1641,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     }
     ra.splits = fill_splits;
     ra.pair_smem_off = static_cast<int64_t>(pair_off);
+    ra.snap = snap_mode ? x.ws<int32_t>(13, static_cast<size_t>(M) * (fill_splits + 1) * N) : nullptr;
     ra.colw = colw;
     {
       // column bands: when A and B together overflow a comfortable share of L2
@@ -1589,6 +1698,13 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
                       : row_threads == 512 ? k_row_count<512>
                                            : k_row_count<256>;
       ensure_dyn_smem(reinterpret_cast<const void*>(count_fn), sm1);
+      if (ra.snap) {
+        const size_t smn = 4 * static_cast<size_t>(N);
+        ensure_dyn_smem(reinterpret_cast<const void*>(k_row_count_split<256>), smn);
+        k_row_count_split<256><<<static_cast<unsigned>(M * fill_splits), 256, smn, st>>>(ra);
+        check_launch("row_count_split");
+        count_launch(&x);
+      }
       count_fn<<<static_cast<unsigned>(M), row_threads, sm1, st>>>(ra);
       check_launch("row_count");
       count_launch(&x);

@@ -140,13 +140,17 @@ def test_k_panels_one_launch(oracle, ctx, monkeypatch, npanels, bs):
         assert np.array_equal(got[("1", eps)].vals, got[("0", eps)].vals)
 
 
+@pytest.mark.parametrize("snap", ["1", "0"])
 @pytest.mark.parametrize("splits,sort_min", [(2, 48), (3, 48), (5, 100000), (8, 48)])
-def test_fill_splits(oracle, ctx, monkeypatch, splits, sort_min):
+def test_fill_splits(oracle, ctx, monkeypatch, splits, sort_min, snap):
     """Long C rows filled by several CTAs (each a range of A chunks, cursors
     offset by the earlier ranges' pairs) emit the same descriptors: against
     the oracle and bit-identical to one CTA per row.  Rows here hold 150 ..
-    1500 A entries (1 .. 6 chunks of 256), mixed sizes, eps filter, C_in."""
+    1500 A entries (1 .. 6 chunks of 256), mixed sizes, eps filter, C_in.
+    BT_SNAP=1: the ranges' column counts come from pass 1's split-count
+    snapshots (k_row_count_split); 0: every fill CTA recounts its row."""
     monkeypatch.setenv("BT_SORT_MIN", str(sort_min))
+    monkeypatch.setenv("BT_SNAP", snap)
     rng = np.random.default_rng(splits)
     rsz = np.array([5, 13, 23], np.int32)[rng.integers(0, 3, 6)]
     ksz = np.array([4, 20, 23], np.int32)[rng.integers(0, 3, 3000)]
