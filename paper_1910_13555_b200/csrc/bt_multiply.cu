@@ -1579,6 +1579,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     const bool snap_mode = fill_splits > 1 && N <= colw && env_int("BT_SNAP", 1) != 0 &&
                            static_cast<double>(M) * (fill_splits + 1) * static_cast<double>(N) * 4.0 <= 64e6;
     if (snap_mode) row_threads = 256;
+    // (the 512-thread fill's pair caches must fit beside the column arrays)
+    if (row_threads == 512 && row_smem + 16 + 10 * static_cast<size_t>(pair_cap<512>()) > 180 * 1024)
+      row_threads = 256;
     size_t pair_off = 0;
     if (row_threads == 512) {  // the 512-thread fill keeps its pair caches here
       pair_off = (row_smem + 15) & ~size_t(15);
