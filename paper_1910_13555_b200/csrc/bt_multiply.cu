@@ -351,7 +351,7 @@ __device__ int compact_touched(const uint32_t* bits, int nw, int32_t* tcol) {
 
 // Pass 1: per C block-row i -- number of C_out blocks, products, T8 slab size,
 // stored elements, per-class work items, useful flops.
-template <int CH>
+template <int CH, bool SNAP = false>
 __device__ __forceinline__ void row_count_one(const RowArgs& g, const int64_t i) {
   extern __shared__ uint32_t cnt[];
   uint32_t* bits = cnt + g.colw;
@@ -376,7 +376,7 @@ __device__ __forceinline__ void row_count_one(const RowArgs& g, const int64_t i)
   // column chunks (one when the row fits the shared-memory counters)
   for (int64_t j0 = 0; j0 < g.ncols; j0 += g.colw) {
     const int64_t jw = min(g.colw, g.ncols - j0);
-    if (g.snap)  // (candidates and flops were added by k_row_count_split)
+    if constexpr (SNAP)  // (candidates and flops were added by k_row_count_split)
       snap_counts(g, i, cnt, bits, nullptr, 0, true);
     else
       row_products(g, i, cnt, bits, rc, &cand, &mnk, j0, jw);
@@ -443,6 +443,13 @@ __device__ __forceinline__ void row_count_one(const RowArgs& g, const int64_t i)
 template <int CH>
 __global__ void __launch_bounds__(CH) k_row_count(const RowArgs g) {
   row_count_one<CH>(g, blockIdx.x);
+}
+
+// split-count mode, second step: the row sums from the per-range snapshots
+// (its own instantiation: the common pass 1 carries none of it)
+template <int CH>
+__global__ void __launch_bounds__(CH) k_row_count_snap(const RowArgs g) {
+  row_count_one<CH, true>(g, blockIdx.x);
 }
 
 // Split-count mode, first step: CTA (i, s) counts the kept pairs of its range
@@ -1697,9 +1704,19 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     const size_t sm1 = static_cast<size_t>(W) * 8 + 4 * ((W + 31) / 32);
     if (M > 0) {
       // static + dynamic shared memory may exceed the 48 KB default: always opt in
-      auto count_fn = row_threads == 64    ? k_row_count<64>
-                      : row_threads == 512 ? k_row_count<512>
-                                           : k_row_count<256>;
+      // pass 1's CTA width: the fill's, except 128 for short rows that 256-thread
+      // CTAs would spread over more than one wave (c2: 1 463 rows of ~215
+      // pairs, pass 1 + scan 37 -> 29 us; c1's 1 600-pair rows keep 256, c4 64)
+      int ct = row_threads;
+      if (row_threads == 256 && a_per_row * b_per_row <= 512.0 && M >= 6 * x.num_sms) ct = 128;
+      ct = env_int("BT_COUNT_THREADS", ct);
+      if (ra.snap) ct = 256;
+      auto count_fn = ra.snap     ? k_row_count_snap<256>
+                      : ct == 64  ? k_row_count<64>
+                      : ct == 128 ? k_row_count<128>
+                      : ct == 512 ? k_row_count<512>
+                                  : k_row_count<256>;
+      const int count_threads = (ct == 64 || ct == 128 || ct == 512) ? ct : 256;
       ensure_dyn_smem(reinterpret_cast<const void*>(count_fn), sm1);
       if (ra.snap) {
         const size_t smn = 4 * static_cast<size_t>(N);
@@ -1708,7 +1725,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         check_launch("row_count_split");
         count_launch(&x);
       }
-      count_fn<<<static_cast<unsigned>(M), row_threads, sm1, st>>>(ra);
+      count_fn<<<static_cast<unsigned>(M), count_threads, sm1, st>>>(ra);
       check_launch("row_count");
       count_launch(&x);
     }

@@ -451,7 +451,8 @@ def test_dfma_tiny_blocks(oracle, ctx, monkeypatch, case):
 @pytest.mark.parametrize("colmask,sort_min,colw", [(1, 48, 0), (0, 48, 0), (0, 0, 0),
                                                    (0, 100000, 0), (1, 48, 50), (0, 0, 37)])
 def test_row_threads_64_vs_256(oracle, ctx, monkeypatch, colmask, sort_min, colw):
-    """The symbolic passes with 64 and with 256 threads per row (BT_ROW_THREADS):
+    """The symbolic passes with 64 and with 256 threads per row (BT_ROW_THREADS;
+    and pass 1 alone with 128, BT_COUNT_THREADS):
     against the oracle and bit-identical to each other, through every
     emission path, column chunks, C_in and the eps filter.  Rows here hold up
     to 300 A entries (several 64-entry chunks)."""
@@ -468,8 +469,10 @@ def test_row_threads_64_vs_256(oracle, ctx, monkeypatch, colmask, sort_min, colw
     B = oracle.random_matrix(6402, ksz, nsz, 0.1)
     Cin = oracle.random_matrix(6403, rsz, nsz, 0.2)
     out = {}
-    for t in ("64", "256"):
-        monkeypatch.setenv("BT_ROW_THREADS", t)
+    for t in ("64", "256", "256/128"):   # 256/128: 128-thread pass 1 (BT_COUNT_THREADS)
+        monkeypatch.setenv("BT_ROW_THREADS", t.split("/")[0])
+        if "/" in t:
+            monkeypatch.setenv("BT_COUNT_THREADS", t.split("/")[1])
         for eps in (0.0, 30.0):
             want, nprod, _ = oracle.multiply(A, B, Cin, eps)
             a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
@@ -480,6 +483,7 @@ def test_row_threads_64_vs_256(oracle, ctx, monkeypatch, colmask, sort_min, colw
             out[(t, eps)] = got
     for eps in (0.0, 30.0):
         assert np.array_equal(out[("64", eps)].vals, out[("256", eps)].vals)
+        assert np.array_equal(out[("256/128", eps)].vals, out[("256", eps)].vals)
 
 
 @pytest.mark.parametrize("seed", range(24))
