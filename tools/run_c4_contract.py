@@ -14,7 +14,8 @@ exactly run_config's matrix, so the values go in as they are.  Two timings:
               device into ((a,b),(P)) (bt_tensor_remap), then multiplies.
 
 CUDA events on the context stream around each contract() call, L2 flushed.
-Parity of the same contraction at small scale: tests/test_tensor_gpu.py.
+Parity of this contraction at full size (both layouts, against the oracle):
+tests/test_configs_gpu.py::test_c4_through_contract_full_size.
 """
 import argparse
 import json
