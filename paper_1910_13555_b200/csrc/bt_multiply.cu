@@ -45,17 +45,26 @@ constexpr int NSEG = NCLASS * kMaxBands;
 constexpr uint32_t kCinFlag = 0x80000000u;
 
 // Tile classes: 16 DMMA tile shapes (ceil(m/8) in 1..4 -- blocks taller than
-// `tr` rows (24 or 32) are cut in tr-row tiles -- times ceil(n/8) in 1..4) +
-// GENERIC (n > 32 or k > 64).
-__host__ __device__ inline int shape_class(int m, int n, bool dmma_ok, int tr, bool tiny) {
+// `tr` rows (24 or 32) are cut in tr-row tiles -- times ceil(n/8) in 1..4;
+// wide blocks (n > 32) are cut in 32-column tiles of the n/8 = 4 classes) +
+// GENERIC (the CUDA-core kernel: only with wide = false, for n > 32 or k > 64).
+__host__ __device__ inline int shape_class(int m, int n, bool dmma_ok, int tr, bool tiny,
+                                           bool wide) {
   if (tiny && m <= kTinyMax && n <= kTinyMax) return TINY;
-  if (!dmma_ok || n > 32) return GENERIC;
+  if (!dmma_ok || (n > 32 && !wide)) return GENERIC;
   const int mc = m > tr ? tr / 8 : (m + 7) / 8;
-  const int nc = (n + 7) / 8;
+  const int nc = n > 32 ? 4 : (n + 7) / 8;
   return (mc - 1) * 4 + (nc - 1);
 }
-__host__ __device__ inline int class_tiles(int m, int cls, int tr) {
+// work items (C tiles) of one C block: row tiles x column tiles
+__host__ __device__ inline int row_tiles(int m, int cls, int tr) {
   return (cls < GENERIC && m > tr) ? (m + tr - 1) / tr : 1;
+}
+__host__ __device__ inline int col_tiles(int n, int cls) {
+  return (cls < GENERIC && n > 32) ? (n + 31) / 32 : 1;
+}
+__host__ __device__ inline int class_tiles(int m, int n, int cls, int tr) {
+  return row_tiles(m, cls, tr) * col_tiles(n, cls);
 }
 
 __device__ __forceinline__ bool keep_product(const double* na, const double* nb, int32_t e,
@@ -97,6 +106,7 @@ struct RowArgs {
   unsigned long long* wlist_n;   // their count
   int wcap_k, wcap_d;
   bool dmma_ok;
+  bool wide;      // blocks wider than 32 columns in 32-column DMMA tiles (else GENERIC)
   // pass 1 outputs
   int32_t* row_nnz;
   int64_t* row_prod;
@@ -128,6 +138,12 @@ __device__ __forceinline__ int band_of(int64_t j, const RowArgs& g) {
     return static_cast<int>(static_cast<uint32_t>(j * g.nbands) / static_cast<uint32_t>(g.ncols));
   return static_cast<int>((j * g.nbands) / g.ncols);
 }
+
+// The work items of one C block (row tiles of tall_rows rows x 32-column
+// tiles of a wide block) at items[at, at + class_tiles).
+__device__ __forceinline__ void emit_items(const RowArgs& g, unsigned long long at, int m, int n,
+                                           int cls, int64_t c_off, int64_t cin, int64_t p0,
+                                           int np);
 
 // Row walk helpers.  A(i,:) x B(k,:) pairs are enumerated load-balanced: the A
 // entries of a chunk are staged in shared memory with the prefix of their B-row
@@ -327,6 +343,16 @@ __device__ __forceinline__ unsigned long long agg_add(unsigned long long* ctr, i
   return base + v * static_cast<unsigned long long>(__popc(below));
 }
 
+// Adds the work items of one C block to its segment counter; returns the
+// lane's slot.  Blocks up to 32 columns: the count depends on the segment
+// alone (the row's m, the class), so the warp-aggregated add applies; a wide
+// block's count also depends on its n (column tiles): one atomic per lane.
+__device__ __forceinline__ unsigned long long tiles_add(unsigned long long* ctr, int seg, int n,
+                                                        unsigned long long v) {
+  if (n > 32) return atomicAdd(ctr, v);
+  return agg_add(ctr, seg, v);
+}
+
 // Touched columns of the row in ascending order -> tcol[0..n); returns n.
 template <int CH>
 __device__ int compact_touched(const uint32_t* bits, int nw, int32_t* tcol) {
@@ -347,6 +373,28 @@ __device__ int compact_touched(const uint32_t* bits, int nw, int32_t* tcol) {
   if (threadIdx.x == 0) total = run;
   __syncthreads();
   return total;
+}
+
+__device__ __forceinline__ void emit_items(const RowArgs& g, unsigned long long at, int m, int n,
+                                           int cls, int64_t c_off, int64_t cin, int64_t p0,
+                                           int np) {
+  const int nr = row_tiles(m, cls, g.tall_rows), nc = col_tiles(n, cls);
+  const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
+  for (int qr = 0; qr < nr; ++qr) {
+    const int r0 = g.tall_rows * qr;
+    for (int qc = 0; qc < nc; ++qc) {
+      const int64_t o = (r0 >> 3) * tile_row + static_cast<int64_t>(qc) * 4 * 64;
+      Item it;
+      it.c_off = c_off + o;
+      it.cin_off = cin >= 0 ? cin + o : -1;
+      it.p0r8 = item_pack(p0, r0 >> 3, 4 * qc);
+      it.np = np;
+      it.rows = static_cast<int16_t>(nr > 1 ? min(g.tall_rows, m - r0) : m);
+      it.n = static_cast<int16_t>(n);
+      BT_DASSERT(static_cast<int64_t>(at) + qr * nc + qc < g.nitems_total, "work item slot");
+      g.items[at + qr * nc + qc] = it;
+    }
+  }
 }
 
 // Pass 1: per C block-row i -- number of C_out blocks, products, T8 slab size,
@@ -390,10 +438,10 @@ __device__ __forceinline__ void row_count_one(const RowArgs& g, const int64_t i)
       prods += v & ~kCinFlag;
       vals += t8_size(m, n);
       elems += static_cast<long long>(m) * n;
-      const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
+      const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny, g.wide);
       const int seg = cls * kMaxBands + band_of(j, g);
-      agg_add(&cls_items[seg], seg,
-              static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
+      tiles_add(&cls_items[seg], seg, n,
+              static_cast<unsigned long long>(class_tiles(m, n, cls, g.tall_rows)));
     }
     __syncthreads();  // counters are cleared for the next chunk
   }
@@ -628,10 +676,10 @@ __device__ __forceinline__ void row_fill_one(const RowArgs& g, const int64_t i, 
         g.out_p0[c] = pbase + run_prod + p_ex;
         cur[j] = static_cast<int32_t>(run_prod + p_ex);
         cnt[j] = static_cast<uint32_t>(run_q + q);  // rank of the C entry in the row
-        const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
+        const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny, g.wide);
         const int seg = cls * kMaxBands + band_of(jg, g);
-        agg_add(&cls_n[seg], seg,
-                static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows)));
+        tiles_add(&cls_n[seg], seg, static_cast<int>(n),
+                static_cast<unsigned long long>(class_tiles(m, n, cls, g.tall_rows)));
       }
       run_prod += p_tot;
       run_val += v_tot;
@@ -823,24 +871,11 @@ __device__ __forceinline__ void row_fill_one(const RowArgs& g, const int64_t i, 
   for (int32_t c = cbase + threadIdx.x; c < g.out_rp[i + 1]; c += blockDim.x) {
     const int j = g.out_col[c];
     const int n = g.n_sz[j];
-    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
-    const int nt = class_tiles(m, cls, g.tall_rows);
+    const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny, g.wide);
+    const int nt = class_tiles(m, n, cls, g.tall_rows);
     const int seg = cls * kMaxBands + band_of(j, g);
-    const unsigned long long at = agg_add(&cls_at[seg], seg, static_cast<unsigned long long>(nt));
-    const int64_t cin = g.cin_map[c];
-    const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
-    for (int q = 0; q < nt; ++q) {
-      const int r0 = g.tall_rows * q;
-      Item it;
-      it.c_off = g.out_off[c] + (r0 >> 3) * tile_row;
-      it.cin_off = cin >= 0 ? cin + (r0 >> 3) * tile_row : -1;
-      it.p0r8 = g.out_p0[c] | (static_cast<int64_t>(r0 >> 3) << 48);
-      it.np = g.out_np[c];
-      it.rows = static_cast<int16_t>(nt > 1 ? min(g.tall_rows, m - r0) : m);
-      it.n = static_cast<int16_t>(n);
-      BT_DASSERT(static_cast<int64_t>(at) + q < g.nitems_total, "work item slot");
-      g.items[at + q] = it;
-    }
+    const unsigned long long at = tiles_add(&cls_at[seg], seg, n, static_cast<unsigned long long>(nt));
+    emit_items(g, at, m, n, cls, g.out_off[c], g.cin_map[c], g.out_p0[c], g.out_np[c]);
   }
   }  // split == 0
 }
@@ -1098,10 +1133,10 @@ __global__ void __launch_bounds__(kWRows * 32) k_wrow_fill(const RowArgs g, cons
         g.out_np[c] = np;
         g.out_p0[c] = pbase + p_ex;
         hkey[s] = static_cast<uint32_t>(p_ex);
-        const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
+        const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny, g.wide);
         const int seg = cls * kMaxBands + band_of(col, g);
         dl[r] = static_cast<uint32_t>(
-            agg_add(&cls_n[seg], seg, static_cast<unsigned long long>(class_tiles(m, cls, g.tall_rows))));
+            tiles_add(&cls_n[seg], seg, static_cast<int>(n), static_cast<unsigned long long>(class_tiles(m, n, cls, g.tall_rows))));
       }
       run_p += __shfl_sync(0xffffffffu, pi, 31);
       run_v += __shfl_sync(0xffffffffu, vi, 31);
@@ -1146,23 +1181,11 @@ __global__ void __launch_bounds__(kWRows * 32) k_wrow_fill(const RowArgs g, cons
       const int cin_l = static_cast<int>(hc >> 8) - 1;
       const int64_t c_off = vbase + run_v + vi - tv;
       const int64_t cin = cin_l >= 0 ? g.c_off[ci0 + cin_l] : -1;
-      const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny);
-      const int nt = class_tiles(m, cls, g.tall_rows);
+      const int cls = shape_class(m, n, g.dmma_ok, g.tall_rows, g.tiny, g.wide);
       const int seg = cls * kMaxBands + band_of(col, g);
       const unsigned long long at = cls_at[seg] + dl[r];
-      const int64_t tile_row = static_cast<int64_t>(tiles8(n)) * 64;
-      for (int q = 0; q < nt; ++q) {
-        const int rt = g.tall_rows * q;
-        Item it;
-        it.c_off = c_off + (rt >> 3) * tile_row;
-        it.cin_off = cin >= 0 ? cin + (rt >> 3) * tile_row : -1;
-        it.p0r8 = (pbase + static_cast<int64_t>(hkey[s])) | (static_cast<int64_t>(rt >> 3) << 48);
-        it.np = static_cast<int32_t>(hc & 0xffu);
-        it.rows = static_cast<int16_t>(nt > 1 ? min(g.tall_rows, m - rt) : m);
-        it.n = static_cast<int16_t>(n);
-        BT_DASSERT(static_cast<int64_t>(at) + q < g.nitems_total, "warp-row work item slot");
-        g.items[at + q] = it;
-      }
+      emit_items(g, at, m, n, cls, c_off, cin, pbase + static_cast<int64_t>(hkey[s]),
+                 static_cast<int>(hc & 0xffu));
     }
     run_v += __shfl_sync(0xffffffffu, vi, 31);
   }
@@ -1179,8 +1202,8 @@ __global__ void k_panel_items(const Item* __restrict__ base, int64_t nitems,
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= nitems) return;
   const Item it = base[t];
-  const int64_t p0 = it.p0r8 & ((int64_t(1) << 48) - 1);
-  const int64_t r8 = it.p0r8 >> 48;
+  const int64_t p0 = item_p0(it);
+  const int r8 = item_r8(it), c8 = item_c8(it);
   int64_t lo = p0;
   for (int p = 0; p < npanels; ++p) {
     // first product with k >= kb[p+1]
@@ -1190,7 +1213,7 @@ __global__ void k_panel_items(const Item* __restrict__ base, int64_t nitems,
       if (desc[mid].w < kb[p + 1]) a = mid + 1; else b = mid;
     }
     Item q = it;
-    q.p0r8 = lo | (r8 << 48);
+    q.p0r8 = item_pack(lo, r8, c8);
     q.np = static_cast<int32_t>(a - lo);
     if (p > 0) q.cin_off = it.c_off;
     out[p * nitems + t] = q;
@@ -1618,7 +1641,15 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     }
 
     const int kmax = A.max_c;
-    const bool dmma_ok = kmax <= 64;
+    // WIDE DMMA path: blocks wider than 32 columns as
+    // 32-column tiles, k of any size in slices -- every block on the tensor
+    // cores.  BT_WIDE=0 (or blocks beyond the item encoding) keeps the
+    // CUDA-core generic kernel for n > 32 or k > 64.
+    const bool wide = env_int("BT_WIDE", 1) != 0 && Cm.max_c <= 8 * kItemMaxC8 &&
+                      Cm.max_r <= 8 * kItemMaxR8;
+    const bool dmma_ok = wide || kmax <= 64;
+    // the WIDE kernel is launched only when some block needs it
+    const bool wide_k = wide && (Cm.max_c > 32 || kmax > 64);
     RowArgs ra{};
     ra.a_rp = A.row_ptr.p;
     ra.a_col = A.col.p;
@@ -1637,6 +1668,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     ra.eps = eps;
     ra.ncols = N;
     ra.dmma_ok = dmma_ok;
+    ra.wide = wide;
     ra.sort_min = env_int("BT_SORT_MIN", 48);
     ra.colmask = colmask;
     ra.tall_rows = env_int("BT_TALL_ROWS", 32) == 24 ? 24 : 32;
@@ -1780,7 +1812,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
     S.flops = 2.0 * static_cast<double>(h.tot[1]);
     S.products = nprod;
     const int64_t nelems = static_cast<int64_t>(h.tot[2]);
-    BT_REQUIRE(nprod < (int64_t(1) << 47), BT_ERR_INVALID_ARGUMENT, "too many products");
+    BT_REQUIRE(nprod < (int64_t(1) << kItemP0Bits), BT_ERR_INVALID_ARGUMENT, "too many products");
     BT_REQUIRE(A.nvals / 64 < (int64_t(1) << 31) && B.nvals / 64 < (int64_t(1) << 31),
                BT_ERR_INVALID_ARGUMENT, "multiply: operand slab exceeds 2^31 tiles");
 
@@ -1929,7 +1961,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
           only = q;
           ++present;
         }
-      const bool fused = npanels > 1 && present == 1 && only < GENERIC &&
+      const bool fused = npanels > 1 && present == 1 && only < GENERIC && !wide_k &&
                          env_int("BT_PANEL_FUSE", 1) != 0;
       if (fused) {
         const int q = only;
@@ -1978,7 +2010,8 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
           maxm = std::max(maxm, q / 4 + 1);
           maxn = std::max(maxn, q % 4 + 1);
         }
-      const bool multi = nclasses > 1 && maxm > 0 && env_int("BT_MULTI", 1) != 0;
+      // (wide_k: every DMMA class in one WIDE launch, even a single class)
+      const bool multi = maxm > 0 && (wide_k || (nclasses > 1 && env_int("BT_MULTI", 1) != 0));
       const bool fork = nclasses > 1;
       const int nstreams = std::min(nclasses, Ctx::kAux);
       if (fork) {
@@ -1986,9 +2019,11 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
         for (int a = 0; a < nstreams; ++a) BT_CUDA(cudaStreamWaitEvent(x.aux[a], x.ev_fork, 0));
       }
       if (multi) {
-        int pcls = 0;
-        KernelFn fn = dmma_multi_kernel(maxm, maxn, pcls);
-        const Plan P = plan_dmma(pcls, ktmax);  // stage plan of the largest tile
+        int pcls = 15;
+        KernelFn fn = wide_k ? k_smm_dmma<4, 4, kWarps, 1, true, false, true>
+                             : dmma_multi_kernel(maxm, maxn, pcls);
+        // stage plan of the largest tile (WIDE: k slices of <= kKTCap tiles)
+        const Plan P = plan_dmma(pcls, wide_k ? std::min(ktmax, kKTCap) : ktmax);
         g.stages = 1;
         g.stage_doubles = P.stage_doubles;
         g.a_region = P.a_region;
@@ -2002,7 +2037,7 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
                                                (g.nitems + kWarps - 1) / kWarps);
         g.ticket_batch = ticket_batch(g.nitems, grid * kWarps,
                                       static_cast<double>(nprod) / std::max<int64_t>(nitems, 1));
-        fn<<<static_cast<unsigned>(grid), kWarps * 32, smem, x.aux[0]>>>(g);
+        fn<<<static_cast<unsigned>(grid), kWarps * 32, smem, fork ? x.aux[0] : st>>>(g);
         check_launch("smm_dmma_multi");
         count_launch(&x);
       }

@@ -24,15 +24,22 @@
 
 namespace bt {
 
-// One C tile of work: rows [r0, r0 + rows) of C block (i, j).  32 bytes.
+// One C tile of work: rows [r0, r0 + rows) x columns [c0, c0 + 32) of C block
+// (i, j) (c0 = 0 and all columns unless the block is wider than 32).  32 bytes.
 struct Item {
-  int64_t c_off;    // element offset of the tile's first row in the C_out slab
+  int64_t c_off;    // element offset of the tile's first 8x8 tile in the C_out slab
   int64_t cin_off;  // same for C_in, or -1
-  int64_t p0r8;     // first product (low 48 bits) | (r0 / 8) << 48
+  int64_t p0r8;     // first product (bits 0-43) | r0 / 8 (bits 44-56) | c0 / 8 (bits 57-63)
   int32_t np;       // number of products
   int16_t rows;     // rows in this tile (<= TM)
-  int16_t n;        // C block columns (row stride)
+  int16_t n;        // C block columns (the block's, not the tile's)
 };
+constexpr int kItemP0Bits = 44;
+constexpr int kItemMaxR8 = (1 << 13) - 1;  // rows of a block <= 65 528
+constexpr int kItemMaxC8 = (1 << 7) - 1;   // columns of a wide block <= 1 016
+__host__ __device__ inline int64_t item_pack(int64_t p0, int r8, int c8) {
+  return p0 | (static_cast<int64_t>(r8) << kItemP0Bits) | (static_cast<int64_t>(c8) << 57);
+}
 
 // Product descriptor: offsets of the A and B blocks in units of one 8x8 tile
 // (64 doubles) and the number of 4-wide k chunks.
@@ -74,11 +81,14 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ int64_t item_p0(const Item& it) {
-  return it.p0r8 & ((int64_t(1) << 48) - 1);
+__host__ __device__ __forceinline__ int64_t item_p0(const Item& it) {
+  return it.p0r8 & ((int64_t(1) << kItemP0Bits) - 1);
 }
-__device__ __forceinline__ int item_r8(const Item& it) {
-  return static_cast<int>(it.p0r8 >> 48);
+__host__ __device__ __forceinline__ int item_r8(const Item& it) {
+  return static_cast<int>((static_cast<uint64_t>(it.p0r8) >> kItemP0Bits) & kItemMaxR8);
+}
+__host__ __device__ __forceinline__ int item_c8(const Item& it) {
+  return static_cast<int>((static_cast<uint64_t>(it.p0r8) >> 57) & kItemMaxC8);
 }
 
 // FP64 DMMA tile kernel: warp <-> C tile of up to TM = 8*TMT rows and exactly
@@ -107,7 +117,14 @@ constexpr int dmma_min_blocks() {
 // PANELS: every K panel of a single-class multiply in one launch (NumArgs
 // npanels / panel_stride / tile_flag); a separate instantiation so the common
 // path carries none of its bookkeeping.
-template <int TMT, int TNT, int WARPS, int S, bool MULTI = false, bool PANELS = false>
+// WIDE (with MULTI): blocks wider than 32 columns arrive as 32-column tiles
+// (item c8: the tile's first 8-column tile; the C and B rows are strided by
+// the block's tile columns) and products with more than kKTCap k tiles are
+// staged in k slices of <= kKTCap tiles, each its own stage (stage_kc bit 8
+// marks a product's last slice): the DMMA path then takes every block size.
+constexpr int kKTCap = 4;
+template <int TMT, int TNT, int WARPS, int S, bool MULTI = false, bool PANELS = false,
+          bool WIDE = false>
 __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_smm_dmma(const NumArgs g) {
   constexpr int QN = 8;     // item slots per warp
   constexpr int CTL = 1536; // control block bytes per warp
@@ -199,6 +216,9 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
   int64_t p_pos = 0, p_end = 0;
   int p_r8 = 0, p_mt = 0;
   int p_nt = TNT;  // B tile columns of the item being issued (MULTI: per item)
+  // WIDE: the block's tile columns, the tile's first tile column, the stage's
+  // B row stride (the tile body's CN), the k slice of the product being issued
+  int p_ntf = TNT, p_c8 = 0, p_cs = TNT, p_sub = 0;
   bool p_more = true;
 
   // next chunk after (item seq n, desc index pos) -- returns false if unknown yet
@@ -286,7 +306,15 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         p_end = p_pos + it.np;
         p_r8 = item_r8(it);
         p_mt = (it.rows + 7) >> 3;
-        if constexpr (MULTI) p_nt = (it.n + 7) >> 3;
+        if constexpr (WIDE) {
+          p_ntf = (it.n + 7) >> 3;
+          p_c8 = item_c8(it);
+          p_cs = p_ntf < 4 ? p_ntf : 4;  // the class width (4 for a wide block)
+          p_nt = p_ntf - p_c8 < 4 ? p_ntf - p_c8 : 4;
+          p_sub = 0;
+        } else if constexpr (MULTI) {
+          p_nt = (it.n + 7) >> 3;
+        }
         ++qt;
         if (p_pos < p_end) enter_chunk(qt - 1, p_pos, p_end);
         continue;
@@ -294,6 +322,55 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
       if (p_pos - c_base >= 32) enter_chunk(qt - 1, p_pos, p_end);
       const int s = s_issue;
       s_issue = (s_issue + 1 == S) ? 0 : s_issue + 1;
+      if constexpr (WIDE) {
+        // every lane reads the descriptor: the slice bookkeeping is warp-uniform
+        const Desc d = dring[cs * 32 + static_cast<int>(p_pos - c_base)];
+        const int KTF = (d.z + 1) >> 1;  // the product's 8-wide k tiles
+        const int h0 = p_sub * kKTCap;
+        const int KTS = KTF - h0 < kKTCap ? KTF - h0 : kKTCap;
+        const int kcs = d.z - 2 * h0 < 2 * kKTCap ? d.z - 2 * h0 : 2 * kKTCap;
+        const bool last = h0 + KTS >= KTF;
+        if (lane == 0) {
+          const uint32_t ba = static_cast<uint32_t>(p_mt * KTS) * 512u;
+          const uint32_t bb = static_cast<uint32_t>(KTS * p_nt) * 512u;
+          double* st = stages + static_cast<int64_t>(s) * g.stage_doubles;
+          stage_kc[s] = kcs | (last ? 0x100 : 0);
+          fence_proxy_async_smem();
+          BT_DASSERT((static_cast<int64_t>(d.x) + static_cast<int64_t>(p_r8 + p_mt) * KTF) * 64 <=
+                         g.a_len, "A slab range (wide)");
+          BT_DASSERT((static_cast<int64_t>(d.y) + static_cast<int64_t>(KTF) * p_ntf) * 64 <= g.b_len,
+                     "B slab range (wide)");
+          BT_DASSERT(p_mt * KTS * 64 <= g.a_region &&
+                         g.a_region + KTS * p_cs * 64 <= g.stage_doubles, "stage capacity (wide)");
+          mbar_arrive_expect_tx(&bars[s], ba + bb);
+          // A: rows r8.. of the block, k tiles [h0, h0 + KTS) (one copy when whole rows)
+          const double* a0 = g.at + (static_cast<int64_t>(d.x) + static_cast<int64_t>(p_r8) * KTF + h0) * 64;
+          if (KTS == KTF) {
+            bulk_g2s(st, a0, ba, &bars[s]);
+          } else {
+            for (int tm = 0; tm < p_mt; ++tm)
+              bulk_g2s(st + tm * KTS * 64, a0 + static_cast<int64_t>(tm) * KTF * 64,
+                       static_cast<uint32_t>(KTS) * 512u, &bars[s]);
+          }
+          // B: k tiles [h0, h0 + KTS) x tile columns [c8, c8 + p_nt), rows p_cs apart
+          const double* b0 = g.bt + (static_cast<int64_t>(d.y) + static_cast<int64_t>(h0) * p_ntf + p_c8) * 64;
+          if (p_nt == p_ntf && p_nt == p_cs) {
+            bulk_g2s(st + g.a_region, b0, bb, &bars[s]);
+          } else {
+            for (int kt = 0; kt < KTS; ++kt)
+              bulk_g2s(st + g.a_region + kt * p_cs * 64, b0 + static_cast<int64_t>(kt) * p_ntf * 64,
+                       static_cast<uint32_t>(p_nt) * 512u, &bars[s]);
+          }
+        }
+        ++issued;
+        if (last) {
+          ++p_pos;
+          p_sub = 0;
+        } else {
+          ++p_sub;
+        }
+        continue;
+      }
       if (lane == 0) {
         const Desc d = dring[cs * 32 + static_cast<int>(p_pos - c_base)];
         const int KT = (d.z + 1) >> 1;  // 8-wide k tiles
@@ -362,15 +439,20 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
           acc[tm][tn][0] = 0.0;
           acc[tm][tn][1] = 0.0;
         }
+      // C rows are RS 8x8 tiles apart (the block's tile columns; CN unless a
+      // WIDE item is a 32-column tile of a wider block, which has NTI tiles)
+      const int RS = WIDE ? (it.n + 7) >> 3 : CN;
+      const int NTI = WIDE ? (RS - item_c8(it) < CN ? RS - item_c8(it) : CN) : CN;
       if (it.cin_off >= 0) {
 #pragma unroll
         for (int tm = 0; tm < CM; ++tm)
           if (tm < mt) {
 #pragma unroll
             for (int tn = 0; tn < CN; ++tn) {
+              if (WIDE && tn >= NTI) continue;
               // PANELS: L2 loads, the tile may have been stored by another SM
               const double2* src = reinterpret_cast<const double2*>(
-                  cin + it.cin_off + ((tm * CN + tn) << 6) + lc);
+                  cin + it.cin_off + ((tm * RS + tn) << 6) + lc);
               const double2 v = PANELS ? __ldcg(src) : *src;
               acc[tm][tn][0] = v.x;
               acc[tm][tn][1] = v.y;
@@ -378,13 +460,17 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
           }
       }
       for (int t = 0; t < it.np; ++t) {
+       bool last_slice = false;
+       while (!last_slice) {  // (one pass unless WIDE splits the product's k)
         const int s = s_cons;
         mbar_wait(&bars[s], cons_phase);
         if (++s_cons == S) {
           s_cons = 0;
           cons_phase ^= 1u;
         }
-        const int kc = stage_kc[s];
+        const int kcw = stage_kc[s];
+        const int kc = WIDE ? (kcw & 0xff) : kcw;
+        last_slice = WIDE ? (kcw >> 8) != 0 : true;
         const int KT = (kc + 1) >> 1;
         const double* sA = stages + static_cast<int64_t>(s) * g.stage_doubles;
         const double* sB = sA + g.a_region;
@@ -424,20 +510,24 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         __syncwarp();
         ++consumed;
         top_up();
+       }
       }
       double* dst = g.cout + it.c_off;
-      BT_DASSERT(it.c_off >= 0 && it.c_off + static_cast<int64_t>(mt) * CN * 64 <= g.cout_len,
+      BT_DASSERT(it.c_off >= 0 &&
+                     it.c_off + (static_cast<int64_t>(mt - 1) * RS + NTI) * 64 <= g.cout_len,
                  "C tile range");
-      BT_DASSERT(it.cin_off < 0 || it.cin_off + static_cast<int64_t>(mt) * CN * 64 <=
+      BT_DASSERT(it.cin_off < 0 || it.cin_off + (static_cast<int64_t>(mt - 1) * RS + NTI) * 64 <=
                                        (cin == g.cout ? g.cout_len : g.cin_len),
                  "C_in tile range");
 #pragma unroll
       for (int tm = 0; tm < CM; ++tm)
         if (tm < mt) {
 #pragma unroll
-          for (int tn = 0; tn < CN; ++tn)
-            __stcs(reinterpret_cast<double2*>(dst + ((tm * CN + tn) << 6) + lc),
+          for (int tn = 0; tn < CN; ++tn) {
+            if (WIDE && tn >= NTI) continue;
+            __stcs(reinterpret_cast<double2*>(dst + ((tm * RS + tn) << 6) + lc),
                    make_double2(acc[tm][tn][0], acc[tm][tn][1]));
+          }
         }
       if constexpr (PANELS) {  // publish: this panel of the tile is stored
         __threadfence();
@@ -446,7 +536,13 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
       }
     };
     if constexpr (MULTI) {
-      const int cls = (mt - 1) * 4 + (((it.n + 7) >> 3) - 1);
+      // (WIDE: every tile of a wide block runs the 32-column body, the last,
+      // narrower one with its columns beyond the block unstored -- measured:
+      // dispatching it on its own width, a 40-column block's last tile on the
+      // 8-column body with 4 accumulator chains, made big40 1.05 -> 1.85 ms)
+      int ntc = (it.n + 7) >> 3;
+      if (WIDE && ntc > 4) ntc = 4;
+      const int cls = (mt - 1) * 4 + (ntc - 1);
       using std::integral_constant;
 #define BT_TILE(cm, cn)                                                   \
   case (cm - 1) * 4 + (cn - 1):                                           \

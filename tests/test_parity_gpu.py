@@ -563,3 +563,49 @@ def test_warp_row_symbolic(oracle, ctx, monkeypatch, h, seed):
         out[mode] = got
     assert np.array_equal(out["0"].bi, out[h].bi) and np.array_equal(out["0"].bj, out[h].bj)
     assert np.array_equal(out["0"].vals, out[h].vals)
+
+
+@pytest.mark.parametrize("case", ["n40_k40", "n64_k64", "n100_k130", "mixed_tall", "panels", "wide_cin_eps"])
+def test_wide_blocks_dmma(oracle, ctx, monkeypatch, case):
+    """Blocks wider than 32 columns and k > 64 on the DMMA path (BT_WIDE=1:
+    32-column C tiles, k sliced in <= 4 tiles per stage) and on the CUDA-core
+    generic kernel (BT_WIDE=0), both against the oracle: C tiles of partial
+    width, k slices of partial depth, tall rows (169), narrow blocks mixed in,
+    C_in, the eps filter, K panels (one WIDE launch per panel)."""
+    from paper_1910_13555_b200.store import multiply_local
+    rng = np.random.default_rng(hash(case) % 2 ** 32)
+    eps, scale, occ_c = 0.0, 0.0, 0.0
+    if case == "n40_k40":
+        rsz = ksz = nsz = np.full(30, 40, np.int32)
+    elif case == "n64_k64":
+        rsz = ksz = nsz = np.full(24, 64, np.int32)
+    elif case == "n100_k130":
+        rsz = np.array([37, 100, 64], np.int32)[rng.integers(0, 3, 12)]
+        ksz = np.array([130, 70, 9], np.int32)[rng.integers(0, 3, 12)]
+        nsz = np.array([100, 41, 33], np.int32)[rng.integers(0, 3, 12)]
+    elif case == "mixed_tall":
+        rsz = np.array([169, 23, 5, 40], np.int32)[rng.integers(0, 4, 16)]
+        ksz = np.array([13, 48, 80], np.int32)[rng.integers(0, 3, 20)]
+        nsz = np.array([5, 13, 23, 40, 72], np.int32)[rng.integers(0, 5, 18)]
+    elif case == "panels":
+        monkeypatch.setenv("BT_KPANELS", "3")
+        rsz = nsz = np.full(10, 48, np.int32)
+        ksz = np.full(60, 40, np.int32)
+    else:   # wide_cin_eps
+        rsz = np.array([40, 20], np.int32)[rng.integers(0, 2, 20)]
+        ksz = np.array([36, 72], np.int32)[rng.integers(0, 2, 20)]
+        nsz = np.array([33, 64, 8], np.int32)[rng.integers(0, 3, 20)]
+        eps, scale, occ_c = 1e-3, 6.0, 0.3
+    A = oracle.random_matrix(8100, rsz, ksz, 0.3, scale)
+    B = oracle.random_matrix(8101, ksz, nsz, 0.3, scale)
+    Cin = oracle.random_matrix(8102, rsz, nsz, occ_c, scale)
+    want, nprod, flops = oracle.multiply(A, B, Cin, eps)
+    for mode in ("1", "0"):
+        monkeypatch.setenv("BT_WIDE", mode)
+        a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+        st = multiply_local(ctx, a, b, c, eps)
+        assert st["products"] == nprod and st["flops"] == flops
+        assert_parity(from_store(c), want)
+        # the whole T8 slots are written (zero padding): norms read it
+        cn = oracle.norms(want)
+        assert np.max(np.abs(c.norms() - cn) / np.maximum(cn, 1e-300)) <= 1e-12
