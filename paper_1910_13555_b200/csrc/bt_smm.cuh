@@ -474,6 +474,39 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         const int KT = (kc + 1) >> 1;
         const double* sA = stages + static_cast<int64_t>(s) * g.stage_doubles;
         const double* sB = sA + g.a_region;
+        // (WIDE) one 8-wide k tile: two 4-wide k chunks (the second may be padding)
+        auto ktile = [&](int kt) {
+          double af[2][CM], bf[2][CN];
+#pragma unroll
+          for (int tm = 0; tm < CM; ++tm) {
+            af[0][tm] = sA[((tm * KT + kt) << 6) + la0];
+            af[1][tm] = sA[((tm * KT + kt) << 6) + la1];
+          }
+#pragma unroll
+          for (int tn = 0; tn < CN; ++tn) {
+            bf[0][tn] = sB[((kt * CN + tn) << 6) + lb0];
+            bf[1][tn] = sB[((kt * CN + tn) << 6) + lb1];
+          }
+#pragma unroll
+          for (int tm = 0; tm < CM; ++tm)
+#pragma unroll
+            for (int tn = 0; tn < CN; ++tn)
+              dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[0][tm], bf[0][tn]);
+          if (2 * kt + 1 < kc) {
+#pragma unroll
+            for (int tm = 0; tm < CM; ++tm)
+#pragma unroll
+              for (int tn = 0; tn < CN; ++tn)
+                dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[1][tm], bf[1][tn]);
+          }
+        };
+        if constexpr (WIDE) {
+          // not unrolled: the WIDE launch carries all 16 tile bodies and items
+          // of several widths, and unrolled bodies overflowed the instruction
+          // cache (ncu: 27-72 % of stall samples on "no instructions")
+#pragma unroll 1
+          for (int kt = 0; kt < KT; ++kt) ktile(kt);
+        } else {
         // k tiles, unrolled by 4 with uniform guards (KT <= 8 for DMMA classes)
         for (int kt0 = 0; kt0 < KT; kt0 += 4) {
 #pragma unroll
@@ -506,6 +539,7 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
               }
             }
           }
+        }
         }
         __syncwarp();
         ++consumed;
