@@ -500,10 +500,13 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
                 dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[1][tm], bf[1][tn]);
           }
         };
-        if constexpr (WIDE) {
-          // not unrolled: the WIDE launch carries all 16 tile bodies and items
-          // of several widths, and unrolled bodies overflowed the instruction
-          // cache (ncu: 27-72 % of stall samples on "no instructions")
+        if constexpr (WIDE || MULTI) {
+          // not unrolled: a MULTI / WIDE launch carries up to 16 tile bodies
+          // (the producer inlined into each) and items of several shapes; the
+          // unrolled bodies overflowed the instruction cache (ncu, WIDE: 27-72 %
+          // of stall samples on "no instructions").  Measured: big40 1.05 ->
+          // 0.84 ms, c2 numeric 102 -> 96 us, c4 3.00 -> 2.96 ms; the
+          // single-class launches (c1, c3) keep the unrolled loop
 #pragma unroll 1
           for (int kt = 0; kt < KT; ++kt) ktile(kt);
         } else {
