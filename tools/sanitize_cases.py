@@ -4,7 +4,8 @@ run):
 
   compute-sanitizer --tool racecheck python tools/sanitize_cases.py
 
-Paths: k_smm_dmma single class, MULTI (mixed sizes, one launch), PANELS (K
+Paths: k_smm_dmma single class, MULTI (mixed sizes, one launch), WIDE (blocks
+wider than 32 / k > 64), the warp-row fill, PANELS (K
 panels in one launch: cross-CTA acquire/release flags), generic (n > 32),
 the eps filter + norms, column-chunked symbolic passes, split fill CTAs, the
 asynchronous export, the tensor remap.  Inputs: numpy, seeded; no checking
@@ -58,7 +59,12 @@ def main():
         env={"BT_KPANELS": "3"})                                             # PANELS fused
     run(ctx, rng, mix(10), mix(60), mix(10), env={"BT_KPANELS": "3"})       # panels per launch
     run(ctx, rng, np.array([37, 40, 5], np.int32), np.array([13, 40], np.int32),
-        np.array([37, 8], np.int32), occ=0.8)                                # generic
+        np.array([37, 8], np.int32), occ=0.8, env={"BT_WIDE": "0"})          # generic
+    run(ctx, rng, np.array([37, 100, 5], np.int32), np.array([13, 70, 130], np.int32),
+        np.array([41, 8, 64], np.int32), occ=0.8)                            # WIDE (tiles, k slices)
+    run(ctx, rng, u(8, 48), u(40, 40), u(8, 48), occ=0.5,
+        env={"BT_KPANELS": "3"})                                             # WIDE per panel
+    run(ctx, rng, mix(40), mix(40), mix(40), occ=0.02, env={"BT_WARP_ROWS": "256"})  # warp-row fill
     run(ctx, rng, mix(8), mix(300), mix(200), occ=0.1, env={"BT_COLW": "40"})   # column chunks
     run(ctx, rng, mix(6), mix(2000), mix(30), occ=0.2, env={"BT_FILL_SPLITS": "3"})  # split fill
     c = run(ctx, rng, mix(30), mix(30), mix(30))
