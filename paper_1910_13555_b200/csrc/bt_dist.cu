@@ -443,6 +443,7 @@ struct Grid {
   int first = 0, nlocal = 1;
   bool nccl = false;
   cudaStream_t comm = nullptr;
+  cudaStream_t comm_vals = nullptr;  // the value all-gather's stream (second communicator)
   cudaEvent_t ev_comm = nullptr, ev_main = nullptr, ev_idx = nullptr;
   std::vector<Counters> totals;
   std::vector<std::map<std::string, Counters>> phases;
@@ -1201,16 +1202,33 @@ cudaEvent_t gather_rows_allgather(Grid& g, const Mat& mine, const std::vector<in
   BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL, std::string("NCCL index gather: ") + ncclGetErrorString(r));
   BT_CUDA(cudaEventRecord(g.ev_idx, cs));
   if (phases) BT_CUDA(cudaEventRecord(pev[2], cs));
+  // values: on a second communicator and stream, concurrent with the index
+  // gather (on one communicator NCCL serialises them: the values started only
+  // once the index had landed).  The communicator is split off the context's
+  // on the first gather (a collective call: every rank is here).
+  cudaStream_t vs = cs;
+  ncclComm_t vcomm = comm;
+  if (env_int("BT_GATHER_2COMM", 1) != 0 && g.comm_vals) {
+    if (!x.nccl_vals) {
+      ncclComm_t c2 = nullptr;
+      ncclResult_t rs = ncclCommSplit(comm, 0, me, &c2, nullptr);
+      BT_REQUIRE(rs == ncclSuccess, BT_ERR_NCCL, std::string("ncclCommSplit: ") + ncclGetErrorString(rs));
+      x.nccl_vals = c2;
+    }
+    vcomm = static_cast<ncclComm_t>(x.nccl_vals);
+    vs = g.comm_vals;
+    BT_CUDA(cudaStreamWaitEvent(vs, g.ev_main, 0));
+  }
   if (maxv) {
     if (sv)
       BT_CUDA(cudaMemcpyAsync(full.vals.p + maxv * me, mine.vals.p, 8 * sv,
-                              cudaMemcpyDeviceToDevice, cs));
-    r = ncclAllGather(full.vals.p + maxv * me, full.vals.p, maxv, ncclFloat64, comm, cs);
+                              cudaMemcpyDeviceToDevice, vs));
+    r = ncclAllGather(full.vals.p + maxv * me, full.vals.p, maxv, ncclFloat64, vcomm, vs);
     BT_REQUIRE(r == ncclSuccess, BT_ERR_NCCL,
                std::string("NCCL value gather: ") + ncclGetErrorString(r));
   }
-  BT_CUDA(cudaEventRecord(g.ev_comm, cs));
-  if (phases) BT_CUDA(cudaEventRecord(pev[4], cs));
+  BT_CUDA(cudaEventRecord(g.ev_comm, vs));
+  if (phases) BT_CUDA(cudaEventRecord(pev[4], vs));
   tr.mark("enqueue rounds");
   BT_CUDA(cudaStreamWaitEvent(x.stream, g.ev_idx, 0));
   if (spec) {  // the headers of the landed index segments, for gather_check
@@ -1492,6 +1510,7 @@ int bt_grid_create(bt_ctx* ctx, int nranks, bt_grid** out) {
       G.first = x.rank;
       G.nlocal = 1;
       BT_CUDA(cudaStreamCreateWithFlags(&G.comm, cudaStreamNonBlocking));
+      BT_CUDA(cudaStreamCreateWithFlags(&G.comm_vals, cudaStreamNonBlocking));
     } else {
       G.first = 0;
       G.nlocal = nranks;
@@ -1515,6 +1534,10 @@ int bt_grid_destroy(bt_grid* g) {
     if (G.comm) {
       cudaStreamSynchronize(G.comm);
       cudaStreamDestroy(G.comm);
+    }
+    if (G.comm_vals) {
+      cudaStreamSynchronize(G.comm_vals);
+      cudaStreamDestroy(G.comm_vals);
     }
     if (G.ev_comm) cudaEventDestroy(G.ev_comm);
     if (G.ev_main) cudaEventDestroy(G.ev_main);

@@ -122,6 +122,9 @@ struct Ctx {
   size_t smem_optin = 227 * 1024;
   int64_t kernels = 0;  // kernels launched through this context
   void* nccl = nullptr; // ncclComm_t when nranks > 1
+  // a second communicator of the same ranks (ncclCommSplit, made by the first
+  // case-2 gather): the B value all-gather runs on it beside the index gather
+  void* nccl_vals = nullptr;
   DBuf<unsigned char> scratch;  // CUB temp storage, reused
   // small mapped page-locked staging for scalar readbacks; layout (bytes):
   //   [0, 1200)      the multiply's sizes block / the export's chunk offsets

@@ -549,6 +549,7 @@ int bt_ctx_destroy(bt_ctx* c) {
     x.scratch.release();
     for (auto& w : x.ws_slots) w.release();
     cudaStreamSynchronize(x.stream);
+    if (x.nccl_vals) ncclCommDestroy(static_cast<ncclComm_t>(x.nccl_vals));
     if (x.nccl) ncclCommDestroy(static_cast<ncclComm_t>(x.nccl));
     if (x.pinned) cudaFreeHost(x.pinned);
     if (x.hstage) cudaFreeHost(x.hstage);
