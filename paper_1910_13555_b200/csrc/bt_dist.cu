@@ -800,9 +800,10 @@ void add_stats(bt_stats& acc, const bt_stats& s) {
 
 void rank_multiply(Ctx* ctx, const Mat& a, const Mat& b, Mat& c, double eps, bt_stats& acc,
                    cudaEvent_t wait_numeric = nullptr, cudaEvent_t numeric_start = nullptr,
-                   const std::function<void()>* after_sizes = nullptr) {
+                   const std::function<void()>* after_sizes = nullptr, bool poll_sizes = false) {
   bt_stats s{};
-  local_multiply(*ctx, a, b, c, eps, &s, wait_numeric, numeric_start, after_sizes);
+  local_multiply(*ctx, a, b, c, eps, &s, wait_numeric, numeric_start, after_sizes, true,
+                 poll_sizes);
   add_stats(acc, s);
 }
 
@@ -1406,8 +1407,12 @@ void case2(const DMat& a, const DMat& b, DMat& c, int nprocs, int gather, double
         cudaEvent_t vals_ready = gather_rows_allgather(g, mine, ks, nprocs, full, spec);
         try {
           std::function<void()> check = [&] { gather_check(g, mine, nprocs, full, true); };
+          // the pass-1 sizes by polling the mapped flag: nothing else of this
+          // call is in flight but the already-enqueued all-gathers (4 GPUs:
+          // 0.859 -> 0.835 ms per bench step; in Cannon, next to its shifts,
+          // polling was slower -- DESIGN.md 4.2)
           rank_multiply(g.ctx, al.view->store(r), full, cl->store(r), eps, S, vals_ready,
-                        g.phase_ev, spec ? &check : nullptr);
+                        g.phase_ev, spec ? &check : nullptr, true);
           break;
         } catch (const SpecMiss&) {
           spec = false;  // a slab outgrew its segment: redo exactly (capacities grow)
