@@ -609,3 +609,36 @@ def test_wide_blocks_dmma(oracle, ctx, monkeypatch, case):
         # the whole T8 slots are written (zero padding): norms read it
         cn = oracle.norms(want)
         assert np.max(np.abs(c.norms() - cn) / np.maximum(cn, 1e-300)) <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_sweep_new_paths(oracle, ctx, monkeypatch, seed):
+    """Randomised shapes through the round-2 paths together: block sizes up to
+    100 (WIDE column tiles, k slices), tall rows, and per seed one of the
+    symbolic variants forced (warp-row fill with either hash size, split-count
+    fill, 128-thread pass 1), C_in and the eps filter -- against the oracle."""
+    from paper_1910_13555_b200.store import multiply_local
+    rng = np.random.default_rng(9100 + seed)
+    variant = [("BT_WARP_ROWS", "128"), ("BT_WARP_ROWS", "256"), ("BT_FILL_SPLITS", "3"),
+               ("BT_COUNT_THREADS", "128")][seed % 4]
+    monkeypatch.setenv(*variant)
+
+    def pal(hi):
+        return rng.choice(np.arange(1, hi + 1), size=int(rng.integers(1, 4)), replace=False)
+
+    pm, pk, pn = pal(100), pal(100), pal(100)
+    if seed % 3 == 0:
+        pm = np.append(pm, 169)
+    rsz = rng.choice(pm, int(rng.integers(2, 40))).astype(np.int32)
+    ksz = rng.choice(pk, int(rng.integers(2, 300 if variant[0] == "BT_FILL_SPLITS" else 60))).astype(np.int32)
+    nsz = rng.choice(pn, int(rng.integers(2, 40))).astype(np.int32)
+    scale = float(rng.choice([0.0, 6.0]))
+    A = oracle.random_matrix(9200 + seed, rsz, ksz, float(rng.choice([0.05, 0.2, 0.6])), scale)
+    B = oracle.random_matrix(9300 + seed, ksz, nsz, float(rng.choice([0.05, 0.2, 0.5])), scale)
+    Cin = oracle.random_matrix(9400 + seed, rsz, nsz, float(rng.choice([0.0, 0.3])), scale)
+    eps = 1e-3 if scale else 0.0
+    want, nprod, flops = oracle.multiply(A, B, Cin, eps)
+    a, b, c = to_store(ctx, A), to_store(ctx, B), to_store(ctx, Cin)
+    st = multiply_local(ctx, a, b, c, eps)
+    assert st["products"] == nprod and st["flops"] == flops
+    assert_parity(from_store(c), want)
