@@ -1640,6 +1640,9 @@ void bt::local_multiply(Ctx& x, const Mat& A, const Mat& B, Mat& Cm, double eps,
       nb = B.norms(st);
     }
 
+    // work items address row tiles of 8 in 13 bits (bt_smm.cuh Item)
+    BT_REQUIRE(Cm.max_r <= 8 * kItemMaxR8, BT_ERR_INVALID_ARGUMENT,
+               "multiply: blocks taller than 65 528 rows are not supported");
     const int kmax = A.max_c;
     // WIDE DMMA path: blocks wider than 32 columns as
     // 32-column tiles, k of any size in slices -- every block on the tensor
