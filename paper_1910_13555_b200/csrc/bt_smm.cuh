@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
         const int KT = (kc + 1) >> 1;
         const double* sA = stages + static_cast<int64_t>(s) * g.stage_doubles;
         const double* sB = sA + g.a_region;
-        // (WIDE) one 8-wide k tile: two 4-wide k chunks (the second may be padding)
+        // one 8-wide k tile: two 4-wide k chunks (the second may be padding)
         auto ktile = [&](int kt) {
           double af[2][CM], bf[2][CN];
 #pragma unroll
@@ -500,50 +500,16 @@ __global__ void __launch_bounds__(WARPS * 32, (dmma_min_blocks<TMT, TNT>())) k_s
                 dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[1][tm], bf[1][tn]);
           }
         };
-        if constexpr (WIDE || MULTI) {
-          // not unrolled: a MULTI / WIDE launch carries up to 16 tile bodies
-          // (the producer inlined into each) and items of several shapes; the
-          // unrolled bodies overflowed the instruction cache (ncu, WIDE: 27-72 %
-          // of stall samples on "no instructions").  Measured: big40 1.05 ->
-          // 0.84 ms, c2 numeric 102 -> 96 us, c4 3.00 -> 2.96 ms; the
-          // single-class launches (c1, c3) keep the unrolled loop
+        // k tiles, not unrolled (at most 8 per product, 4 per WIDE slice).
+        // Measured against the loop unrolled by 4 with uniform guards: the
+        // MULTI / WIDE launches carry up to 16 tile bodies (the producer
+        // inlined into each) and the unrolled bodies overflowed the
+        // instruction cache (ncu, WIDE: 27-72 % of stall samples on "no
+        // instructions"; big40 1.05 -> 0.84 ms, c2 numeric 102 -> 96 us, c4
+        // 3.00 -> 2.96 ms), and even the single-body launches run faster
+        // rolled (c1 numeric 0.594 -> 0.585 ms, c3 1.751 -> 1.677 ms)
 #pragma unroll 1
-          for (int kt = 0; kt < KT; ++kt) ktile(kt);
-        } else {
-        // k tiles, unrolled by 4 with uniform guards (KT <= 8 for DMMA classes)
-        for (int kt0 = 0; kt0 < KT; kt0 += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int kt = kt0 + u;
-            if (kt < KT) {
-              // two 4-wide k chunks per 8x8 tile column (the second may be padding)
-              double af[2][CM], bf[2][CN];
-#pragma unroll
-              for (int tm = 0; tm < CM; ++tm) {
-                af[0][tm] = sA[((tm * KT + kt) << 6) + la0];
-                af[1][tm] = sA[((tm * KT + kt) << 6) + la1];
-              }
-#pragma unroll
-              for (int tn = 0; tn < CN; ++tn) {
-                bf[0][tn] = sB[((kt * CN + tn) << 6) + lb0];
-                bf[1][tn] = sB[((kt * CN + tn) << 6) + lb1];
-              }
-#pragma unroll
-              for (int tm = 0; tm < CM; ++tm)
-#pragma unroll
-                for (int tn = 0; tn < CN; ++tn)
-                  dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[0][tm], bf[0][tn]);
-              if (2 * kt + 1 < kc) {
-#pragma unroll
-                for (int tm = 0; tm < CM; ++tm)
-#pragma unroll
-                  for (int tn = 0; tn < CN; ++tn)
-                    dmma_884(acc[tm][tn][0], acc[tm][tn][1], af[1][tm], bf[1][tn]);
-              }
-            }
-          }
-        }
-        }
+        for (int kt = 0; kt < KT; ++kt) ktile(kt);
         __syncwarp();
         ++consumed;
         top_up();
