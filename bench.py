@@ -40,8 +40,8 @@ SEED_A, SEED_B = 1001, 1002
 FP64_PEAK_TFLOPS = 37.1   # measured: tools/microbench/fp64_peak.cu on B200 (profiles/)
 # dram__bytes_read.sum + dram__bytes_write.sum of one k_smm_dmma launch on this
 # workload, from `ncu --set full` of this bench (profiles/r02/ncu_bench_dmma_summary.txt):
-# 0.594 GB read + 0.694 GB written (algorithmic: 0.80 GB)
-NCU_TRAFFIC_BYTES = 1.2886e9
+# 0.646 GB read + 0.697 GB written (algorithmic: 0.80 GB)
+NCU_TRAFFIC_BYTES = 1.3422e9
 
 
 METRIC = "block-sparse FP64 useful GFLOP/s"
